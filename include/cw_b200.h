@@ -1,0 +1,133 @@
+/*
+ * cw_b200.h -- C ABI of the B200-native per-pixel whitening pipeline
+ * (arXiv 1408.3526; drop-in for the reference `clutterwhiten` hot path).
+ *
+ * The reference has no native boundary: its hot path is the Python call
+ * `Pipeline.process_frame(frame) -> WhitenedOutput | None`
+ * (/root/reference/pkg/src/clutterwhiten/pipeline.py:201-294), which drives
+ * 13 numba kernels through `BlockExecutor.map_blocks(fn, n)`
+ * (parallel.py:62-73, _kernels.py:31-342).  This library replaces that
+ * whole operator layer (L0 + L1 in SURVEY.md §1) with one fused sm_100a
+ * kernel per frame behind the entry points below; the Python host layer
+ * (`paper_1408_3526_b200.pipeline.Pipeline`) binds them with ctypes and
+ * keeps the reference's Python signature.  Plain pointers and sizes only:
+ * no torch or C++ types cross this boundary, no exceptions, every call
+ * returns a status (CW_OK == 0, < 0 on error; text via cw_last_error).
+ */
+#ifndef CW_B200_H
+#define CW_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CW_ABI_VERSION 1
+
+enum cw_status {
+    CW_OK = 0,
+    CW_ERR_PARAM = -1,     /* maps to ParamError (params.py:30) */
+    CW_ERR_VALUE = -2,     /* maps to ValueError */
+    CW_ERR_CUDA = -3,      /* CUDA runtime failure (no CPU fallback exists) */
+    CW_ERR_NOMEM = -4,     /* device allocation failed */
+    CW_ERR_UNSUPPORTED = -5 /* geometry without a compiled kernel instance */
+};
+
+/* FilterParams (params.py:34-63); lags as float64 like the reference. */
+typedef struct cw_params {
+    int32_t kx, ky, kz;      /* half windows: M = 2K + 1 */
+    int32_t bx, by;          /* half bandwidths, B < K */
+    int32_t mhat[3];         /* group delay (mhat_x, mhat_y, mhat_z) */
+    double alpha;            /* smoothing pole in (0, 1) */
+    int32_t n_lag_x, n_lag_y;
+    const double *lag_x;     /* strictly increasing fractional lags (px) */
+    const double *lag_y;
+} cw_params;
+
+typedef struct cw_handle cw_handle;
+
+/*
+ * Create a stream pipeline for (width x height) frames on CUDA `device`.
+ * `bank_c64` is FilterBank.coeffs (design.py:208-253) as interleaved
+ * float32 (re, im) pairs, shape (Ly, Lx, retained); `retained` is
+ * retained_bin_indices (design.py:195-205).  Replaces Pipeline.__init__
+ * (pipeline.py:118-177) minus the host-side bank design.
+ * `halo_rows` / `row_offset` describe a spatial strip (multi-GPU): the
+ * first `halo_rows` local rows are input-only, and local row 0 is global
+ * row `row_offset` (both 0 for a whole frame).
+ */
+int cw_create(const cw_params *params, int32_t width, int32_t height, int32_t device,
+              const float *bank_c64, const int64_t *retained, int32_t n_retained,
+              int32_t halo_rows, int32_t row_offset, cw_handle **out);
+
+void cw_destroy(cw_handle *h);
+
+/* Last error message of this handle (or of the failed create when h is NULL). */
+const char *cw_last_error(const cw_handle *h);
+
+/* Override every pixel's velocity with grid index (ix, iy); (-1, -1) clears.
+ * Replaces the forced_velocity branch of pipeline.py:174-177, 260-265. */
+int cw_set_forced_velocity(cw_handle *h, int32_t ix, int32_t iy);
+
+/*
+ * Push one frame: the whole SpectrumStream.push + conditioning + flow +
+ * PEF chain of Pipeline.process_frame (pipeline.py:201-294).
+ *  frame        : (H, W) float32, HOST memory (pinned gives async copies)
+ *  residual     : (H, W) float32 host out, or NULL
+ *  prediction   : (H, W) float32 host out, or NULL
+ *  vidx         : (H, W, 2) uint8 host out [ix, iy] per anchor, or NULL
+ *  ready        : 1 when an output frame was produced (frames_seen >= Mz)
+ *  frame_index  : input index of the output frame (n - mhat_z)
+ *  stream       : cudaStream_t to run on (NULL: the handle's own stream)
+ * Synchronises `stream` before returning when any host output is given.
+ */
+int cw_push(cw_handle *h, const float *frame, float *residual, float *prediction, uint8_t *vidx,
+            int32_t *ready, int64_t *frame_index, void *stream);
+
+/* Same, with the frame already in device memory and outputs left on the
+ * device (see cw_device_outputs); never synchronises. */
+int cw_push_device(cw_handle *h, const float *frame_dev, int32_t *ready, int64_t *frame_index,
+                   void *stream);
+
+/* Device pointers of the latest outputs: residual (H,W) f32, prediction
+ * (H,W) f32, vidx (H,W,2) u8.  Valid until the next push. */
+int cw_device_outputs(cw_handle *h, float **residual, float **prediction, uint8_t **vidx);
+
+/* Device pointer of the frame-ring slot the next push will use (for
+ * producers that write frames in place, e.g. NCCL halo receives). */
+int cw_next_frame_slot(cw_handle *h, float **slot);
+
+/* Push the frame already written into cw_next_frame_slot(). */
+int cw_push_inplace(cw_handle *h, int32_t *ready, int64_t *frame_index, void *stream);
+
+int64_t cw_frames_seen(const cw_handle *h);
+
+/* Enable/disable the parity dump of the spectrum S (observer output). */
+int cw_set_debug(cw_handle *h, int32_t on);
+
+/*
+ * Parity views (tests only), copied to host after synchronising:
+ *  what = 0: spectrum S of the last frame, (H, W, Mz, My, Mx) complex128
+ *            (reference SpectrumField.bins layout, spectrum.py:107-135;
+ *            requires cw_set_debug(h, 1) before the push)
+ *  what = 1: smoothed kz-collapsed state T^ (H, W, My, Mx) complex128
+ *            (R^ = autocorr of T^, flow.py:87-114)
+ *  what = 2: raw observer state, float32, kernel layout
+ * `bytes` must equal the view size; returns CW_ERR_VALUE otherwise.
+ */
+int cw_read_view(cw_handle *h, int32_t what, void *dst, size_t bytes);
+
+/* Kernel-only timing support: number of CUDA kernels one push launches
+ * and the grid/block shape of the frame kernel (bench.py bookkeeping). */
+int cw_launch_info(const cw_handle *h, int32_t *kernels_per_push, int32_t *grid, int32_t *block,
+                   int32_t *smem_bytes);
+
+/* Library/ABI identification. */
+int32_t cw_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CW_B200_H */

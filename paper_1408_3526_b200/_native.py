@@ -1,0 +1,139 @@
+"""ctypes binding of the C ABI in include/cw_b200.h (libcw_b200.so).
+
+This is the only way the package reaches the device: there is no CPU
+fallback.  If the shared library is missing or no CUDA device exists, the
+calls raise ``NativeUnavailable`` -- loudly, never silently.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+from .params import ParamError
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_ROOT = os.path.dirname(_PKG)
+LIB_PATH = os.path.join(_PKG, "libcw_b200.so")
+CSRC = os.path.join(_PKG, "csrc")
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17",
+    "-Xcompiler", "-fPIC", "-shared",
+]
+
+CW_OK, CW_ERR_PARAM, CW_ERR_VALUE, CW_ERR_CUDA, CW_ERR_NOMEM, CW_ERR_UNSUPPORTED = 0, -1, -2, -3, -4, -5
+
+#: every symbol include/cw_b200.h declares (checked by tests/test_abi.py)
+EXPORTS = (
+    "cw_abi_version", "cw_create", "cw_destroy", "cw_last_error", "cw_set_forced_velocity",
+    "cw_push", "cw_push_device", "cw_device_outputs", "cw_next_frame_slot", "cw_push_inplace",
+    "cw_frames_seen", "cw_set_debug", "cw_read_view", "cw_launch_info",
+)
+
+
+class NativeUnavailable(RuntimeError):
+    """The CUDA library or a CUDA device is missing (no fallback exists)."""
+
+
+class NativeError(RuntimeError):
+    """A CUDA-side failure reported through the C ABI."""
+
+
+def build(verbose: bool = False) -> str:
+    """Compile csrc/cw_api.cu for sm_100a into libcw_b200.so (nvcc)."""
+    cmd = ["nvcc", *NVCC_FLAGS, "-o", LIB_PATH, os.path.join(CSRC, "cw_api.cu")]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+    subprocess.run(cmd, check=True)
+    return LIB_PATH
+
+
+class cw_params(ctypes.Structure):
+    _fields_ = [
+        ("kx", ctypes.c_int32), ("ky", ctypes.c_int32), ("kz", ctypes.c_int32),
+        ("bx", ctypes.c_int32), ("by", ctypes.c_int32),
+        ("mhat", ctypes.c_int32 * 3),
+        ("alpha", ctypes.c_double),
+        ("n_lag_x", ctypes.c_int32), ("n_lag_y", ctypes.c_int32),
+        ("lag_x", ctypes.POINTER(ctypes.c_double)), ("lag_y", ctypes.POINTER(ctypes.c_double)),
+    ]
+
+
+_lib = None
+
+
+def load():
+    """Load libcw_b200.so and declare its prototypes."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise NativeUnavailable(
+            f"{LIB_PATH} is not built; run __graft_entry__.build() (nvcc, sm_100a). "
+            "There is no CPU fallback."
+        )
+    lib = ctypes.CDLL(LIB_PATH)
+    vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+    P = ctypes.POINTER
+    sig = {
+        "cw_abi_version": (i32, []),
+        "cw_create": (ctypes.c_int, [P(cw_params), i32, i32, i32, P(ctypes.c_float), P(i64), i32, i32, i32, P(vp)]),
+        "cw_destroy": (None, [vp]),
+        "cw_last_error": (ctypes.c_char_p, [vp]),
+        "cw_set_forced_velocity": (ctypes.c_int, [vp, i32, i32]),
+        "cw_push": (ctypes.c_int, [vp, P(ctypes.c_float), P(ctypes.c_float), P(ctypes.c_float),
+                                   P(ctypes.c_uint8), P(i32), P(i64), vp]),
+        "cw_push_device": (ctypes.c_int, [vp, vp, P(i32), P(i64), vp]),
+        "cw_device_outputs": (ctypes.c_int, [vp, P(vp), P(vp), P(vp)]),
+        "cw_next_frame_slot": (ctypes.c_int, [vp, P(vp)]),
+        "cw_push_inplace": (ctypes.c_int, [vp, P(i32), P(i64), vp]),
+        "cw_frames_seen": (i64, [vp]),
+        "cw_set_debug": (ctypes.c_int, [vp, i32]),
+        "cw_read_view": (ctypes.c_int, [vp, i32, vp, ctypes.c_size_t]),
+        "cw_launch_info": (ctypes.c_int, [vp, P(i32), P(i32), P(i32), P(i32)]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if lib.cw_abi_version() != 1:
+        raise NativeUnavailable("libcw_b200.so ABI version mismatch; rebuild it")
+    _lib = lib
+    return lib
+
+
+def check(rc: int, handle=None) -> None:
+    """Map a C status to the reference's exception types."""
+    if rc == CW_OK:
+        return
+    msg = (load().cw_last_error(handle) or b"").decode("utf-8", "replace")
+    if rc == CW_ERR_PARAM:
+        raise ParamError(msg)
+    if rc in (CW_ERR_VALUE, CW_ERR_UNSUPPORTED):
+        raise ValueError(msg)
+    if rc == CW_ERR_CUDA and ("no CUDA device" in msg or "cudaSetDevice" in msg):
+        raise NativeUnavailable(msg)
+    raise NativeError(msg)
+
+
+def fptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+
+
+def make_params(params) -> tuple[cw_params, list]:
+    """Pack FilterParams into the C struct (keeps the lag arrays alive)."""
+    lx = np.ascontiguousarray(params.lag_grid_x, dtype=np.float64)
+    ly = np.ascontiguousarray(params.lag_grid_y, dtype=np.float64)
+    cp = cw_params()
+    cp.kx, cp.ky, cp.kz, cp.bx, cp.by = params.kx, params.ky, params.kz, params.bx, params.by
+    cp.mhat = (ctypes.c_int32 * 3)(*params.mhat)
+    cp.alpha = float(params.alpha)
+    cp.n_lag_x, cp.n_lag_y = lx.size, ly.size
+    cp.lag_x = lx.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    cp.lag_y = ly.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    return cp, [lx, ly]

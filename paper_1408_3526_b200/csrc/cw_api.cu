@@ -1,0 +1,680 @@
+// cw_api.cu -- C ABI of the B200 whitening pipeline (include/cw_b200.h).
+//
+// Host side of the drop-in: owns the per-stream device state (observer
+// state, smoothing state T^, raw-frame delay ring, outputs), folds the
+// reference's constant tables into float tables for the fused kernel, and
+// launches one cw_frame_kernel per frame.  Reference counterparts are cited
+// per function; there is no CPU compute path: every frame runs on the GPU
+// or the call fails with CW_ERR_CUDA.
+#include "cw_frame.cuh"
+#include "../../include/cw_b200.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+using namespace cwb;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct LaunchFn {
+    void (*launch)(const FrameArgs &, const Tables &, int grid, cudaStream_t);
+    const void *kernel;
+    int threads;
+    size_t smem;
+    int ns, nt, nret;
+};
+
+template <int KX, int KY, int KZ, int BX, int BY>
+void launch_inst(const FrameArgs &a, const Tables &t, int grid, cudaStream_t s)
+{
+    using G = Geo<KX, KY, KZ, BX, BY>;
+    cw_frame_kernel<G><<<grid, G::NTHREADS, G::SMEM_BYTES, s>>>(a, t);
+}
+
+template <int KX, int KY, int KZ, int BX, int BY>
+LaunchFn make_inst()
+{
+    using G = Geo<KX, KY, KZ, BX, BY>;
+    LaunchFn f;
+    f.launch = &launch_inst<KX, KY, KZ, BX, BY>;
+    f.kernel = reinterpret_cast<const void *>(&cw_frame_kernel<G>);
+    f.threads = G::NTHREADS;
+    f.smem = G::SMEM_BYTES;
+    f.ns = G::NS;
+    f.nt = G::NT;
+    f.nret = G::NRET;
+    return f;
+}
+
+// Compiled geometries: the default (4,4,2,3,3) and the SURVEY §8d C5 sweep.
+bool find_inst(int kx, int ky, int kz, int bx, int by, LaunchFn *out)
+{
+#define CW_INST(a, b, c, d, e)                                                  \
+    if (kx == a && ky == b && kz == c && bx == d && by == e) {                 \
+        *out = make_inst<a, b, c, d, e>();                                      \
+        return true;                                                            \
+    }
+    CW_INST(4, 4, 2, 3, 3)
+    CW_INST(3, 3, 2, 2, 2)
+    CW_INST(5, 5, 2, 4, 4)
+    CW_INST(4, 4, 1, 3, 3)
+    CW_INST(2, 2, 1, 1, 1)
+#undef CW_INST
+    return false;
+}
+
+}  // namespace
+
+struct cw_handle {
+    int kx, ky, kz, bx, by, mhx, mhy, mhz;
+    int mx, my, mz;
+    int W, H, NXB, halo, row_off;
+    int device;
+    int nlx, nly;
+    double alpha;
+    std::vector<double> lag_x, lag_y;
+    LaunchFn fn;
+    Tables tab;
+    int grid;
+    cudaStream_t own = nullptr;
+    float *d_state = nullptr, *d_that = nullptr, *d_coef = nullptr, *d_frames = nullptr;
+    float *d_res = nullptr, *d_pred = nullptr, *d_dbg = nullptr;
+    uint8_t *d_vidx = nullptr;
+    size_t state_floats = 0, that_floats = 0;
+    long long frames_seen = 0;
+    bool have_that = false;
+    bool debug = false;
+    int forced_ix = -1, forced_iy = -1;
+    std::string err;
+};
+
+static int fail(cw_handle *h, int code, const std::string &msg)
+{
+    if (h)
+        h->err = msg;
+    else
+        g_create_error = msg;
+    return code;
+}
+
+#define CW_CUDA(h, expr)                                                                  \
+    do {                                                                                  \
+        cudaError_t _e = (expr);                                                          \
+        if (_e != cudaSuccess)                                                            \
+            return fail((h), CW_ERR_CUDA, std::string(#expr ": ") + cudaGetErrorString(_e)); \
+    } while (0)
+
+// validate(): the subset of params.py:114-158 that the device path relies on
+// (the Python host layer runs the full rule set with the reference messages).
+static int check_params(const cw_params *p, int W, int H, std::string *msg)
+{
+    char buf[256];
+    if (p->kx < 1 || p->ky < 1 || p->kz < 1) {
+        *msg = "half-window sizes must be >= 1";
+        return CW_ERR_PARAM;
+    }
+    if (p->bx < 0 || p->bx >= p->kx || p->by < 0 || p->by >= p->ky) {
+        *msg = "bandwidth must satisfy B < K";
+        return CW_ERR_PARAM;
+    }
+    const int m[3] = {2 * p->kx + 1, 2 * p->ky + 1, 2 * p->kz + 1};
+    for (int i = 0; i < 3; i++)
+        if (p->mhat[i] < 0 || p->mhat[i] > m[i] - 1) {
+            snprintf(buf, sizeof buf, "group delay component %d outside window [0, %d]", p->mhat[i], m[i] - 1);
+            *msg = buf;
+            return CW_ERR_PARAM;
+        }
+    if (!(p->alpha > 0.0 && p->alpha < 1.0)) {
+        *msg = "smoothing pole must be in (0,1)";
+        return CW_ERR_PARAM;
+    }
+    if (p->n_lag_x < 1 || p->n_lag_y < 1 || p->n_lag_x > MAXL || p->n_lag_y > MAXL || !p->lag_x || !p->lag_y) {
+        snprintf(buf, sizeof buf, "lag grids must hold 1..%d entries", MAXL);
+        *msg = buf;
+        return CW_ERR_UNSUPPORTED;
+    }
+    if (W < m[0] || H < m[1]) {
+        snprintf(buf, sizeof buf, "image %dx%d smaller than analysis window %dx%d", W, H, m[0], m[1]);
+        *msg = buf;
+        return CW_ERR_PARAM;
+    }
+    return CW_OK;
+}
+
+// Float tables for the fused kernel (double-precision construction).
+//  x/y phase tables: spectrum.py:65-74; autocorr tables: flow.py:87-97;
+//  pick gains: flow.py:147-163; pick tie order: _kernels.py:286-298.
+static void build_tables(cw_handle *h)
+{
+    Tables &t = h->tab;
+    std::memset(&t, 0, sizeof t);
+    const double PI = 3.14159265358979323846;
+    const int Mx = h->mx, My = h->my, Mz = h->mz;
+    for (int k = 0; k <= h->kx; k++)
+        for (int m = 0; m < Mx; m++) {
+            t.exc[k][m] = (float)std::cos(2 * PI * k * m / Mx);
+            t.exs[k][m] = (float)std::sin(2 * PI * k * m / Mx);
+        }
+    for (int k = 0; k <= h->ky; k++) {
+        for (int m = 0; m < My; m++) {
+            t.eyc[k][m] = (float)std::cos(2 * PI * k * m / My);
+            t.eys[k][m] = (float)std::sin(2 * PI * k * m / My);
+        }
+        t.twc[k] = (float)std::cos(2 * PI * k / My);
+        t.tws[k] = (float)std::sin(2 * PI * k / My);
+    }
+    for (int i = 0; i < Mz; i++) {
+        const int kz = i - h->kz;
+        t.wc[i] = (float)std::cos(2 * PI * kz / Mz);
+        t.ws[i] = (float)std::sin(2 * PI * kz / Mz);
+        t.azc[i] = (float)std::cos(2 * PI * kz / Mz);
+        t.azs[i] = (float)-std::sin(2 * PI * kz / Mz);
+    }
+    std::vector<double> gx(h->nlx), gy(h->nly);
+    for (int i = 0; i < h->nlx; i++)
+        gx[i] = 0.375 / (0.25 + 0.125 * std::cos(2 * PI * h->lag_x[i] / Mx));
+    for (int i = 0; i < h->nly; i++)
+        gy[i] = 0.375 / (0.25 + 0.125 * std::cos(2 * PI * h->lag_y[i] / My));
+    // stage 1: e^{-j 2 pi kx lx / Mx} = cos - j sin, gx folded
+    for (int l = 0; l < h->nlx; l++) {
+        t.s1g[l] = (float)gx[l];
+        for (int k = 1; k <= h->kx; k++) {
+            const double th = 2 * PI * k * h->lag_x[l] / Mx;
+            t.s1c[l][k - 1] = (float)(gx[l] * std::cos(th));
+            t.s1s[l][k - 1] = (float)(gx[l] * std::sin(th));
+        }
+    }
+    // stage 2: R = B0 + 2 sum_ky (cos phi Re B + sin phi Im B), gy folded
+    for (int l = 0; l < h->nly; l++) {
+        t.s2g[l] = (float)gy[l];
+        for (int k = 1; k <= h->ky; k++) {
+            const double ph = 2 * PI * k * h->lag_y[l] / My;
+            t.s2c[l][k - 1] = (float)(2.0 * gy[l] * std::cos(ph));
+            t.s2s[l][k - 1] = (float)(2.0 * gy[l] * std::sin(ph));
+        }
+    }
+    // rank: sort by (lag_x^2 + lag_y^2, ix, iy) -- the reference tie order
+    std::vector<int> order(h->nlx * h->nly);
+    for (int i = 0; i < (int)order.size(); i++)
+        order[i] = i;  // i = iy * nlx + ix
+    auto n2 = [&](int i) {
+        const int ix = i % h->nlx, iy = i / h->nlx;
+        return h->lag_x[ix] * h->lag_x[ix] + h->lag_y[iy] * h->lag_y[iy];
+    };
+    std::sort(order.begin(), order.end(), [&](int a, int b) {
+        const double na = n2(a), nb = n2(b);
+        if (na != nb)
+            return na < nb;
+        const int ax = a % h->nlx, bx = b % h->nlx;
+        if (ax != bx)
+            return ax < bx;
+        return a / h->nlx < b / h->nlx;
+    });
+    for (int rk = 0; rk < (int)order.size(); rk++) {
+        const int i = order[rk];
+        t.rank[i] = (uint16_t)rk;
+        t.rix[rk] = (uint8_t)(i % h->nlx);
+        t.riy[rk] = (uint8_t)(i / h->nlx);
+    }
+    t.cS = (float)(Mz / std::sqrt((double)Mx * My * Mz));
+    t.inv_mz = (float)(1.0 / Mz);
+    t.alpha = (float)h->alpha;
+    t.beta = (float)(1.0 - h->alpha);
+    t.nlx = h->nlx;
+    t.nly = h->nly;
+}
+
+// PEF coefficients on the stored half space (pipeline.py:269-282,
+// _kernels.py:330-342): pred = Re sum_k c(k) S(k) over the retained band,
+// folded so that the kernel computes sum_j coef[j] * xhat+[j] with
+// S = cS * xhat+, pairing k with -k: Re(c S) + Re(c' conj S)
+//   = S.re (c.re + c'.re) + S.im (c'.im - c.im).
+static int build_coef(cw_handle *h, const float *bank, const int64_t *retained, int nret,
+                      std::vector<float> *out)
+{
+    const int Mx = h->mx, My = h->my, Mz = h->mz, KX = h->kx, KY = h->ky, KZ = h->kz;
+    const int BX = h->bx, BY = h->by;
+    const int WX = 2 * BX + 1;
+    // map reference flat bin -> coefficient position j
+    std::vector<int> pos(Mx * My * Mz, -1);
+    for (int j = 0; j < nret; j++) {
+        if (retained[j] < 0 || retained[j] >= Mx * My * Mz)
+            return CW_ERR_VALUE;
+        pos[retained[j]] = j;
+    }
+    auto flat = [&](int kz, int ky, int kx) { return ((kz + KZ) * My + (ky + KY)) * Mx + (kx + KX); };
+    const double cS = Mz / std::sqrt((double)Mx * My * Mz);
+    const int NRET = Mz * WX * (2 * BY + 1);
+    out->assign((size_t)h->nlx * h->nly * NRET, 0.f);
+    for (int v = 0; v < h->nlx * h->nly; v++) {
+        const float *bk = bank + (size_t)v * nret * 2;
+        auto coef = [&](int kz, int ky, int kx, double *re, double *im) -> bool {
+            const int j = pos[flat(kz, ky, kx)];
+            if (j < 0)
+                return false;
+            *re = bk[2 * j];
+            *im = bk[2 * j + 1];
+            return true;
+        };
+        float *o = out->data() + (size_t)v * NRET;
+        int w = 0;
+        auto pair = [&](int kz, int ky, int kx) -> bool {
+            double cr, ci, dr, di;
+            if (!coef(kz, ky, kx, &cr, &ci) || !coef(-kz, -ky, -kx, &dr, &di))
+                return false;
+            o[w++] = (float)(cS * (cr + dr));
+            o[w++] = (float)(cS * (di - ci));
+            return true;
+        };
+        // row 0: DC bin (kz = 0 real, kz = 1..KZ), then kx = 1..BX, all kz
+        double cr, ci;
+        if (!coef(0, 0, 0, &cr, &ci))
+            return CW_ERR_VALUE;
+        o[w++] = (float)(cS * cr);
+        for (int kz = 1; kz <= KZ; kz++)
+            if (!pair(kz, 0, 0))
+                return CW_ERR_VALUE;
+        for (int kx = 1; kx <= BX; kx++)
+            for (int kz = -KZ; kz <= KZ; kz++)
+                if (!pair(kz, 0, kx))
+                    return CW_ERR_VALUE;
+        for (int ky = 1; ky <= BY; ky++)
+            for (int kx = -BX; kx <= BX; kx++)
+                for (int kz = -KZ; kz <= KZ; kz++)
+                    if (!pair(kz, ky, kx))
+                        return CW_ERR_VALUE;
+        if (w != NRET)
+            return CW_ERR_VALUE;
+    }
+    return CW_OK;
+}
+
+extern "C" {
+
+int32_t cw_abi_version(void) { return CW_ABI_VERSION; }
+
+const char *cw_last_error(const cw_handle *h) { return h ? h->err.c_str() : g_create_error.c_str(); }
+
+int cw_create(const cw_params *p, int32_t width, int32_t height, int32_t device, const float *bank_c64,
+              const int64_t *retained, int32_t n_retained, int32_t halo_rows, int32_t row_offset,
+              cw_handle **out)
+{
+    if (!out || !p)
+        return fail(nullptr, CW_ERR_VALUE, "null argument");
+    *out = nullptr;
+    std::string msg;
+    int rc = check_params(p, width, height, &msg);
+    if (rc != CW_OK)
+        return fail(nullptr, rc, msg);
+    LaunchFn fn;
+    if (!find_inst(p->kx, p->ky, p->kz, p->bx, p->by, &fn)) {
+        char buf[200];
+        snprintf(buf, sizeof buf, "no compiled kernel for (kx,ky,kz,bx,by)=(%d,%d,%d,%d,%d)", p->kx, p->ky, p->kz,
+                 p->bx, p->by);
+        return fail(nullptr, CW_ERR_UNSUPPORTED, buf);
+    }
+    const int nret_expect = (2 * p->kz + 1) * (2 * p->bx + 1) * (2 * p->by + 1);
+    if (n_retained != nret_expect || !bank_c64 || !retained)
+        return fail(nullptr, CW_ERR_VALUE, "bank does not match the retained band of these parameters");
+    if (halo_rows < 0 || halo_rows >= height || row_offset < 0)
+        return fail(nullptr, CW_ERR_VALUE, "bad strip geometry");
+
+    cw_handle *h = new cw_handle();
+    h->kx = p->kx;
+    h->ky = p->ky;
+    h->kz = p->kz;
+    h->bx = p->bx;
+    h->by = p->by;
+    h->mhx = p->mhat[0];
+    h->mhy = p->mhat[1];
+    h->mhz = p->mhat[2];
+    h->mx = 2 * p->kx + 1;
+    h->my = 2 * p->ky + 1;
+    h->mz = 2 * p->kz + 1;
+    h->W = width;
+    h->H = height;
+    h->NXB = (width + 31) / 32;
+    h->halo = halo_rows;
+    h->row_off = row_offset;
+    h->device = device;
+    h->nlx = p->n_lag_x;
+    h->nly = p->n_lag_y;
+    h->alpha = p->alpha;
+    h->lag_x.assign(p->lag_x, p->lag_x + p->n_lag_x);
+    h->lag_y.assign(p->lag_y, p->lag_y + p->n_lag_y);
+    h->fn = fn;
+    build_tables(h);
+    std::vector<float> coef;
+    rc = build_coef(h, bank_c64, retained, n_retained, &coef);
+    if (rc != CW_OK) {
+        delete h;
+        return fail(nullptr, rc, "bank/retained layout inconsistent with the parameters");
+    }
+
+    auto cleanup_fail = [&](int code, const std::string &m) {
+        std::string keep = h->err.empty() ? m : h->err;
+        cw_destroy(h);
+        return fail(nullptr, code, keep);
+    };
+    if (cudaSetDevice(device) != cudaSuccess)
+        return cleanup_fail(CW_ERR_CUDA, "cudaSetDevice failed (no CUDA device?)");
+    if (cudaStreamCreateWithFlags(&h->own, cudaStreamNonBlocking) != cudaSuccess)
+        return cleanup_fail(CW_ERR_CUDA, "cudaStreamCreate failed");
+    if (cudaFuncSetAttribute(fn.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fn.smem) != cudaSuccess)
+        return cleanup_fail(CW_ERR_CUDA, "cannot reserve shared memory for the frame kernel");
+    int occ = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn.kernel, fn.threads, fn.smem);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    if (occ < 1 || sms < 1)
+        return cleanup_fail(CW_ERR_CUDA, "frame kernel cannot be resident on this device");
+    const long long units = (long long)h->NXB * (height - halo_rows);
+    h->grid = (int)std::min<long long>((long long)occ * sms, std::max<long long>(1, units / 2));
+
+    const size_t pix_packets = (size_t)height * h->NXB;
+    h->state_floats = pix_packets * fn.ns * 32;
+    h->that_floats = pix_packets * fn.nt * 32;
+    const size_t HW = (size_t)width * height;
+    if (cudaMalloc(&h->d_state, h->state_floats * 4) != cudaSuccess ||
+        cudaMalloc(&h->d_that, h->that_floats * 4) != cudaSuccess ||
+        cudaMalloc(&h->d_coef, coef.size() * 4) != cudaSuccess ||
+        cudaMalloc(&h->d_frames, HW * 4 * (h->mhz + 1)) != cudaSuccess ||
+        cudaMalloc(&h->d_res, HW * 4) != cudaSuccess || cudaMalloc(&h->d_pred, HW * 4) != cudaSuccess ||
+        cudaMalloc(&h->d_vidx, HW * 2) != cudaSuccess)
+        return cleanup_fail(CW_ERR_NOMEM, "device allocation failed");
+    cudaMemsetAsync(h->d_state, 0, h->state_floats * 4, h->own);
+    cudaMemsetAsync(h->d_that, 0, h->that_floats * 4, h->own);
+    cudaMemsetAsync(h->d_frames, 0, HW * 4 * (h->mhz + 1), h->own);
+    cudaMemsetAsync(h->d_res, 0, HW * 4, h->own);
+    cudaMemsetAsync(h->d_pred, 0, HW * 4, h->own);
+    cudaMemsetAsync(h->d_vidx, 0, HW * 2, h->own);
+    cudaMemcpyAsync(h->d_coef, coef.data(), coef.size() * 4, cudaMemcpyHostToDevice, h->own);
+    if (cudaStreamSynchronize(h->own) != cudaSuccess)
+        return cleanup_fail(CW_ERR_CUDA, "device initialisation failed");
+    *out = h;
+    return CW_OK;
+}
+
+void cw_destroy(cw_handle *h)
+{
+    if (!h)
+        return;
+    if (h->own)
+        cudaStreamSynchronize(h->own);
+    cudaFree(h->d_state);
+    cudaFree(h->d_that);
+    cudaFree(h->d_coef);
+    cudaFree(h->d_frames);
+    cudaFree(h->d_res);
+    cudaFree(h->d_pred);
+    cudaFree(h->d_vidx);
+    cudaFree(h->d_dbg);
+    if (h->own)
+        cudaStreamDestroy(h->own);
+    delete h;
+}
+
+int cw_set_forced_velocity(cw_handle *h, int32_t ix, int32_t iy)
+{
+    if (!h)
+        return CW_ERR_VALUE;
+    if (ix < 0 || iy < 0) {
+        h->forced_ix = h->forced_iy = -1;
+        return CW_OK;
+    }
+    if (ix >= h->nlx || iy >= h->nly)
+        return fail(h, CW_ERR_PARAM, "forced velocity index outside the grid");
+    h->forced_ix = ix;
+    h->forced_iy = iy;
+    return CW_OK;
+}
+
+int cw_set_debug(cw_handle *h, int32_t on)
+{
+    if (!h)
+        return CW_ERR_VALUE;
+    h->debug = on != 0;
+    if (h->debug && !h->d_dbg) {
+        CW_CUDA(h, cudaSetDevice(h->device));
+        CW_CUDA(h, cudaMalloc(&h->d_dbg, h->state_floats * 4));
+        CW_CUDA(h, cudaMemset(h->d_dbg, 0, h->state_floats * 4));
+    }
+    return CW_OK;
+}
+
+int64_t cw_frames_seen(const cw_handle *h) { return h ? h->frames_seen : -1; }
+
+int cw_next_frame_slot(cw_handle *h, float **slot)
+{
+    if (!h || !slot)
+        return CW_ERR_VALUE;
+    const size_t HW = (size_t)h->W * h->H;
+    *slot = h->d_frames + (size_t)(h->frames_seen % (h->mhz + 1)) * HW;
+    return CW_OK;
+}
+
+static cudaStream_t pick_stream(cw_handle *h, void *stream)
+{
+    return stream ? reinterpret_cast<cudaStream_t>(stream) : h->own;
+}
+
+// The frame already sits in its ring slot: run the fused kernel.
+static int run_frame(cw_handle *h, cudaStream_t s, int32_t *ready, int64_t *frame_index)
+{
+    const size_t HW = (size_t)h->W * h->H;
+    const long long n = h->frames_seen;
+    const int rd = (n + 1 >= h->mz) ? 1 : 0;
+    FrameArgs a;
+    a.frame = h->d_frames + (size_t)(n % (h->mhz + 1)) * HW;
+    a.delayed = rd ? h->d_frames + (size_t)(((n - h->mhz) % (h->mhz + 1))) * HW : nullptr;
+    a.state = h->d_state;
+    a.that = h->d_that;
+    a.coefP = h->d_coef;
+    a.res = h->d_res;
+    a.pred = h->d_pred;
+    a.vidx = h->d_vidx;
+    a.dbgS = h->debug ? h->d_dbg : nullptr;
+    a.W = h->W;
+    a.H = h->H;
+    a.NXB = h->NXB;
+    a.y_begin = h->halo;
+    a.y_off = h->row_off;
+    a.ready = rd;
+    a.first = (rd && !h->have_that) ? 1 : 0;
+    a.forced_ix = h->forced_ix;
+    a.forced_iy = h->forced_iy;
+    a.mhx = h->mhx;
+    a.mhy = h->mhy;
+    h->fn.launch(a, h->tab, h->grid, s);
+    CW_CUDA(h, cudaGetLastError());
+    h->frames_seen = n + 1;
+    if (rd)
+        h->have_that = true;
+    if (ready)
+        *ready = rd;
+    if (frame_index)
+        *frame_index = rd ? n - h->mhz : -1;
+    return CW_OK;
+}
+
+int cw_push_inplace(cw_handle *h, int32_t *ready, int64_t *frame_index, void *stream)
+{
+    if (!h)
+        return CW_ERR_VALUE;
+    return run_frame(h, pick_stream(h, stream), ready, frame_index);
+}
+
+int cw_push_device(cw_handle *h, const float *frame_dev, int32_t *ready, int64_t *frame_index, void *stream)
+{
+    if (!h || !frame_dev)
+        return CW_ERR_VALUE;
+    cudaStream_t s = pick_stream(h, stream);
+    float *slot;
+    cw_next_frame_slot(h, &slot);
+    const size_t HW = (size_t)h->W * h->H;
+    if (slot != frame_dev)
+        CW_CUDA(h, cudaMemcpyAsync(slot, frame_dev, HW * 4, cudaMemcpyDeviceToDevice, s));
+    return run_frame(h, s, ready, frame_index);
+}
+
+int cw_push(cw_handle *h, const float *frame, float *residual, float *prediction, uint8_t *vidx, int32_t *ready,
+            int64_t *frame_index, void *stream)
+{
+    if (!h || !frame)
+        return CW_ERR_VALUE;
+    cudaStream_t s = pick_stream(h, stream);
+    float *slot;
+    cw_next_frame_slot(h, &slot);
+    const size_t HW = (size_t)h->W * h->H;
+    CW_CUDA(h, cudaMemcpyAsync(slot, frame, HW * 4, cudaMemcpyHostToDevice, s));
+    int32_t rd = 0;
+    int rc = run_frame(h, s, &rd, frame_index);
+    if (rc != CW_OK)
+        return rc;
+    if (ready)
+        *ready = rd;
+    bool sync = false;
+    if (rd) {
+        if (residual) {
+            CW_CUDA(h, cudaMemcpyAsync(residual, h->d_res, HW * 4, cudaMemcpyDeviceToHost, s));
+            sync = true;
+        }
+        if (prediction) {
+            CW_CUDA(h, cudaMemcpyAsync(prediction, h->d_pred, HW * 4, cudaMemcpyDeviceToHost, s));
+            sync = true;
+        }
+        if (vidx) {
+            CW_CUDA(h, cudaMemcpyAsync(vidx, h->d_vidx, HW * 2, cudaMemcpyDeviceToHost, s));
+            sync = true;
+        }
+    }
+    if (sync)
+        CW_CUDA(h, cudaStreamSynchronize(s));
+    return CW_OK;
+}
+
+int cw_device_outputs(cw_handle *h, float **residual, float **prediction, uint8_t **vidx)
+{
+    if (!h)
+        return CW_ERR_VALUE;
+    if (residual)
+        *residual = h->d_res;
+    if (prediction)
+        *prediction = h->d_pred;
+    if (vidx)
+        *vidx = h->d_vidx;
+    return CW_OK;
+}
+
+int cw_launch_info(const cw_handle *h, int32_t *kernels_per_push, int32_t *grid, int32_t *block,
+                   int32_t *smem_bytes)
+{
+    if (!h)
+        return CW_ERR_VALUE;
+    if (kernels_per_push)
+        *kernels_per_push = 1;
+    if (grid)
+        *grid = h->grid;
+    if (block)
+        *block = h->fn.threads;
+    if (smem_bytes)
+        *smem_bytes = (int32_t)h->fn.smem;
+    return CW_OK;
+}
+
+// Parity views: unpack the packet layout into the reference layouts.
+int cw_read_view(cw_handle *h, int32_t what, void *dst, size_t bytes)
+{
+    if (!h || !dst)
+        return CW_ERR_VALUE;
+    CW_CUDA(h, cudaSetDevice(h->device));
+    CW_CUDA(h, cudaDeviceSynchronize());
+    const int W = h->W, H = h->H, NXB = h->NXB;
+    const int Mx = h->mx, My = h->my, Mz = h->mz, KX = h->kx, KY = h->ky, KZ = h->kz;
+    if (what == 2) {
+        if (bytes != h->state_floats * 4)
+            return fail(h, CW_ERR_VALUE, "view size mismatch");
+        CW_CUDA(h, cudaMemcpy(dst, h->d_state, bytes, cudaMemcpyDeviceToHost));
+        return CW_OK;
+    }
+    if (what == 0) {
+        const size_t nb = (size_t)Mx * My * Mz;
+        if (bytes != (size_t)H * W * nb * 16)
+            return fail(h, CW_ERR_VALUE, "view size mismatch");
+        if (!h->d_dbg)
+            return fail(h, CW_ERR_VALUE, "spectrum view needs cw_set_debug(h, 1) before the push");
+        std::vector<float> pk(h->state_floats);
+        CW_CUDA(h, cudaMemcpy(pk.data(), h->d_dbg, h->state_floats * 4, cudaMemcpyDeviceToHost));
+        double *o = static_cast<double *>(dst);
+        const int NS = h->fn.ns;
+        auto put = [&](size_t pixbase, int kz, int ky, int kx, double re, double im) {
+            size_t i = pixbase + (((size_t)(kz + KZ) * My + (ky + KY)) * Mx + (kx + KX));
+            o[2 * i] = re;
+            o[2 * i + 1] = im;
+            size_t j = pixbase + (((size_t)(-kz + KZ) * My + (-ky + KY)) * Mx + (-kx + KX));
+            o[2 * j] = re;
+            o[2 * j + 1] = -im;
+        };
+        for (int y = 0; y < H; y++)
+            for (int x = 0; x < W; x++) {
+                const float *f = pk.data() + ((size_t)y * NXB + x / 32) * NS * 32 + (x % 32);
+                auto F = [&](int j) { return (double)f[(size_t)j * 32]; };
+                const size_t pb = ((size_t)y * W + x) * nb;
+                put(pb, 0, 0, 0, F(0), 0.0);
+                for (int kz = 1; kz <= KZ; kz++)
+                    put(pb, kz, 0, 0, F(1 + 2 * (kz - 1)), F(2 + 2 * (kz - 1)));
+                for (int kx = 1; kx <= KX; kx++)
+                    for (int kz = -KZ; kz <= KZ; kz++) {
+                        const int j = Mz + (kx - 1) * 2 * Mz + 2 * (kz + KZ);
+                        put(pb, kz, 0, kx, F(j), F(j + 1));
+                    }
+                for (int ky = 1; ky <= KY; ky++)
+                    for (int kx = -KX; kx <= KX; kx++)
+                        for (int kz = -KZ; kz <= KZ; kz++) {
+                            const int j = Mz * Mx + (ky - 1) * 2 * Mx * Mz + ((kx + KX) * Mz + (kz + KZ)) * 2;
+                            put(pb, kz, ky, kx, F(j), F(j + 1));
+                        }
+            }
+        return CW_OK;
+    }
+    if (what == 1) {
+        const size_t nt = (size_t)Mx * My;
+        if (bytes != (size_t)H * W * nt * 16)
+            return fail(h, CW_ERR_VALUE, "view size mismatch");
+        std::vector<float> pk(h->that_floats);
+        CW_CUDA(h, cudaMemcpy(pk.data(), h->d_that, h->that_floats * 4, cudaMemcpyDeviceToHost));
+        double *o = static_cast<double *>(dst);
+        const int NT = h->fn.nt;
+        auto put = [&](size_t pb, int ky, int kx, double re, double im) {
+            size_t i = pb + (size_t)(ky + KY) * Mx + (kx + KX);
+            o[2 * i] = re;
+            o[2 * i + 1] = im;
+            size_t j = pb + (size_t)(-ky + KY) * Mx + (-kx + KX);
+            o[2 * j] = re;
+            o[2 * j + 1] = -im;
+        };
+        for (int y = 0; y < H; y++)
+            for (int x = 0; x < W; x++) {
+                const float *f = pk.data() + ((size_t)y * NXB + x / 32) * NT * 32 + (x % 32);
+                auto F = [&](int j) { return (double)f[(size_t)j * 32]; };
+                const size_t pb = ((size_t)y * W + x) * nt;
+                put(pb, 0, 0, F(0), 0.0);
+                for (int kx = 1; kx <= KX; kx++)
+                    put(pb, 0, kx, F(2 * kx - 1), F(2 * kx));
+                for (int ky = 1; ky <= KY; ky++)
+                    for (int kx = -KX; kx <= KX; kx++) {
+                        const int j = Mx + (ky - 1) * 2 * Mx + 2 * (kx + KX);
+                        put(pb, ky, kx, F(j), F(j + 1));
+                    }
+            }
+        return CW_OK;
+    }
+    return fail(h, CW_ERR_VALUE, "unknown view");
+}
+
+}  // extern "C"

@@ -1,0 +1,260 @@
+"""Drop-in ``Pipeline`` for the reference whitening path, running on B200.
+
+Mirrors /root/reference/pkg/src/clutterwhiten/pipeline.py: same
+constructor (118-127), ``process_frame`` contract (201-294: ``None`` during
+the Mz-1 warm-up frames, then a ``WhitenedOutput`` aligned to input index
+``n - mhat_z``), properties, context manager and error behaviour.  Each
+call uploads the frame and runs ONE fused sm_100a kernel through the C ABI
+(include/cw_b200.h); outputs are fresh host arrays per call.
+
+Differences from the reference, by design:
+* ``strategy`` is accepted and reported but never changes results (the
+  device path has one execution shape).
+* ``spectrum_backend="naive"`` (the reference's non-recursive oracle
+  backend, spectrum.py:257-327) is not a device path yet and raises.
+* ``imag_peak`` is 0.0 by construction: the PEF sums conjugate bin pairs,
+  so the prediction is real without a discarded imaginary residue.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .design import FilterBank, FreqKernel, build_bank
+from .flow import VelocityField
+from .parallel import ExecStrategy
+from .params import FilterParams, ParamError, validate
+
+__all__ = ["WhitenedOutput", "Pipeline", "apply_pef", "valid_bounds", "valid_mask"]
+
+
+def valid_bounds(params: FilterParams, width: int, height: int):
+    """Inclusive output bounds (ox_lo, ox_hi, oy_lo, oy_hi) with a full
+    analysis window behind the anchor (pipeline.py:41-50)."""
+    mhx, mhy, _ = params.mhat
+    return (params.mx - 1 - mhx, width - 1 - mhx, params.my - 1 - mhy, height - 1 - mhy)
+
+
+def valid_mask(params: FilterParams, width: int, height: int) -> np.ndarray:
+    """(H, W) bool mask of valid output pixels (pipeline.py:53-58)."""
+    x0, x1, y0, y1 = valid_bounds(params, width, height)
+    mask = np.zeros((height, width), dtype=bool)
+    mask[y0 : y1 + 1, x0 : x1 + 1] = True
+    return mask
+
+
+def apply_pef(bins, kernel, delayed_intensity: float):
+    """One pixel's prediction/residual from its (Mz, My, Mx) bins
+    (host utility, pipeline.py:61-81)."""
+    coeffs = kernel.coeffs if isinstance(kernel, FreqKernel) else np.asarray(kernel)
+    bins = np.asarray(bins, dtype=np.complex128)
+    mz, wy, wx = coeffs.shape
+    if bins.ndim != 3 or bins.shape[0] != mz:
+        raise ValueError(f"bins shape {bins.shape} incompatible with kernel {coeffs.shape}")
+    cy, cx = (bins.shape[1] - 1) // 2, (bins.shape[2] - 1) // 2
+    hy, hx = (wy - 1) // 2, (wx - 1) // 2
+    band = bins[:, cy - hy : cy + hy + 1, cx - hx : cx + hx + 1]
+    pred = float(np.sum(coeffs.astype(np.complex128) * band).real)
+    return pred, float(delayed_intensity) - pred
+
+
+@dataclass
+class WhitenedOutput:
+    """One whitened frame (pipeline.py:84-99)."""
+
+    frame_index: int
+    residual: np.ndarray
+    prediction: np.ndarray
+    velocity: VelocityField
+    mask: np.ndarray
+    imag_peak: float
+
+
+class Pipeline:
+    """Streaming whitening filter for one frame geometry on one GPU.
+
+    Parameters are those of the reference (pipeline.py:102-127) plus
+    ``device`` (CUDA ordinal).
+    """
+
+    def __init__(
+        self,
+        params: FilterParams,
+        width: int,
+        height: int,
+        strategy: ExecStrategy | str = "serial",
+        spectrum_backend: str = "recursive",
+        forced_velocity=None,
+        bank: FilterBank | None = None,
+        device: int = 0,
+        _strip: tuple[int, int] = (0, 0),
+    ):
+        validate(params)
+        if isinstance(strategy, str):
+            strategy = ExecStrategy.parse(strategy)
+        self._strategy = strategy
+        if width < params.mx or height < params.my:
+            raise ParamError(
+                f"image {width}x{height} smaller than analysis window {params.mx}x{params.my}"
+            )
+        if spectrum_backend == "naive":
+            raise ValueError("spectrum backend 'naive' has no device implementation yet")
+        if spectrum_backend != "recursive":
+            raise ValueError(f"unknown spectrum backend {spectrum_backend!r}")
+        self.spectrum_backend = spectrum_backend
+        if bank is None:
+            bank = build_bank(params)
+        elif bank.params != params:
+            raise ParamError("filter bank was built for different parameters")
+        self.params = params
+        self.width = int(width)
+        self.height = int(height)
+        self.bank = bank
+        self.device = int(device)
+        self.mask = valid_mask(params, width, height)
+        self.mask.setflags(write=False)
+        self.last_timings: dict[str, float] = {}
+        self._lag_x = np.asarray(params.lag_grid_x, dtype=np.float64)
+        self._lag_y = np.asarray(params.lag_grid_y, dtype=np.float64)
+
+        self._forced = None
+        if forced_velocity is not None:
+            ix, iy = bank.index_of(forced_velocity)
+            self._forced = (ix, iy)
+
+        lib = _native.load()
+        cparams, self._keep = _native.make_params(params)
+        coeffs = np.ascontiguousarray(bank.coeffs_flat, dtype=np.complex64)
+        retained = np.ascontiguousarray(bank.retained, dtype=np.int64)
+        handle = ctypes.c_void_p()
+        rc = lib.cw_create(
+            ctypes.byref(cparams), self.width, self.height, self.device,
+            _native.fptr(coeffs.view(np.float32)),
+            retained.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), retained.size,
+            int(_strip[0]), int(_strip[1]), ctypes.byref(handle),
+        )
+        _native.check(rc, None)
+        self._h = handle
+        if self._forced is not None:
+            _native.check(lib.cw_set_forced_velocity(self._h, *self._forced), self._h)
+
+    # -- reference properties (pipeline.py:179-199) -------------------------
+
+    @property
+    def strategy(self) -> ExecStrategy:
+        return self._strategy
+
+    @property
+    def latency(self) -> int:
+        return self.params.mhat[2]
+
+    @property
+    def frames_seen(self) -> int:
+        return int(_native.load().cw_frames_seen(self._h))
+
+    def set_strategy(self, strategy: ExecStrategy | str) -> None:
+        """Accepted for compatibility; outputs are unaffected."""
+        self._strategy = ExecStrategy.parse(strategy) if isinstance(strategy, str) else strategy
+
+    # -- the hot entry ---------------------------------------------------------
+
+    def process_frame(self, frame) -> WhitenedOutput | None:
+        """Consume one frame; ``None`` until Mz frames were seen, then the
+        whitened frame ``n - mhat_z`` (pipeline.py:201-294)."""
+        frame = np.ascontiguousarray(frame, dtype=np.float32)
+        if frame.shape != (self.height, self.width):
+            raise ValueError(f"frame shape {frame.shape} != {(self.height, self.width)}")
+        lib = _native.load()
+        t0 = time.perf_counter()
+        h, w = self.height, self.width
+        res = np.empty((h, w), np.float32)
+        pred = np.empty((h, w), np.float32)
+        vidx = np.empty((h, w, 2), np.uint8)
+        ready = ctypes.c_int32(0)
+        fidx = ctypes.c_int64(-1)
+        rc = lib.cw_push(
+            self._h, _native.fptr(frame), _native.fptr(res), _native.fptr(pred),
+            vidx.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)),
+            ctypes.byref(ready), ctypes.byref(fidx), None,
+        )
+        _native.check(rc, self._h)
+        self.last_timings = {"pipeline": time.perf_counter() - t0}
+        if not ready.value:
+            return None
+        idx = vidx.astype(np.int32)
+        vel = np.empty((h, w, 2), np.float64)
+        vel[..., 0] = self._lag_x[idx[..., 0]]
+        vel[..., 1] = self._lag_y[idx[..., 1]]
+        return WhitenedOutput(
+            frame_index=int(fidx.value),
+            residual=res,
+            prediction=pred,
+            velocity=VelocityField(idx, vel),
+            mask=self.mask,
+            imag_peak=0.0,
+        )
+
+    # -- parity views (tests) ------------------------------------------------
+
+    def enable_spectrum_dump(self, on: bool = True) -> None:
+        """Record the observer spectrum S of each frame (tests/parity only)."""
+        _native.check(_native.load().cw_set_debug(self._h, int(bool(on))), self._h)
+
+    def spectrum(self) -> np.ndarray:
+        """S of the last frame as (H, W, Mz, My, Mx) complex128 (reference
+        SpectrumField.bins layout); needs enable_spectrum_dump() first."""
+        p = self.params
+        out = np.zeros((self.height, self.width, p.mz, p.my, p.mx), np.complex128)
+        rc = _native.load().cw_read_view(self._h, 0, out.ctypes.data, out.nbytes)
+        _native.check(rc, self._h)
+        return out
+
+    def smoothed_state(self) -> np.ndarray:
+        """T^ (H, W, My, Mx) complex128: the kz-collapsed smoothed power whose
+        lag transform is the reference R^ (flow.py:87-114)."""
+        p = self.params
+        out = np.zeros((self.height, self.width, p.my, p.mx), np.complex128)
+        rc = _native.load().cw_read_view(self._h, 1, out.ctypes.data, out.nbytes)
+        _native.check(rc, self._h)
+        return out
+
+    def launch_info(self) -> dict:
+        k, g, b, s = (ctypes.c_int32() for _ in range(4))
+        _native.check(_native.load().cw_launch_info(self._h, *(ctypes.byref(v) for v in (k, g, b, s))), self._h)
+        return {"kernels_per_push": k.value, "grid": g.value, "block": b.value, "smem_bytes": s.value}
+
+    # -- lifetime ---------------------------------------------------------------
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _native.load().cw_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+        return False
+
+
+def rhat_from_state(that: np.ndarray, params: FilterParams) -> np.ndarray:
+    """R^(ly, lx) = Re sum_k e^{-j2pi(kx lx/Mx + ky ly/My)} T^(ky, kx): the
+    reference's smoothed autocorrelation recovered from T^ (flow.py:100-114,
+    _kernels.py:230-258 with the kz collapse already applied)."""
+    kx = np.arange(params.mx) - params.kx
+    ky = np.arange(params.my) - params.ky
+    axl = np.exp(-2j * np.pi * np.outer(np.asarray(params.lag_grid_x), kx) / params.mx)
+    ayl = np.exp(-2j * np.pi * np.outer(np.asarray(params.lag_grid_y), ky) / params.my)
+    return np.einsum("lx,my,...yx->...ml", axl, ayl, that).real
