@@ -1,0 +1,369 @@
+#!/usr/bin/env python
+"""Benchmark: pixel-frames/s of the full SDFT -> deadbeat observer -> flow ->
+PEF chain on 640x512 frames (BASELINE.json config C3), with % of the HBM
+roofline.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step is one 640x512 frame through the whole per-pixel pipeline (one
+fused kernel).  ``value`` is measured with the frames already resident in
+HBM (cw_push_device on torch's current stream, CUDA events); ``e2e`` goes
+through the public ``Pipeline.process_frame`` with pinned host frames
+(H2D of the frame + D2H of residual, prediction and velocity per step).
+The per-pixel state (1.6 KB/px, 0.5 GB per stream) is larger than L2, so
+no L2 flush is needed between steps.  Under torchrun (N > 1) every rank runs
+an independent 640x512 sensor stream on its own GPU (streams
+shard with no exchange), timed between barriers, max over ranks.
+
+``--impl reference`` times the reference algorithm on the host cores: the
+float64 C restatement in oracle/ (bit-exact to the reference package, see
+tests/test_oracle_golden.py), all host threads, same config and metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WIDTH, HEIGHT = 640, 512
+METRIC = "pixel-frames/sec (640x512, full pipeline)"
+UNIT = "px-frames/s"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def b_alg(p, with_prediction=True) -> int:
+    """Algorithmic HBM bytes per pixel-frame: frame in, delayed
+    frame, observer state R+W, smoothing state R+W, residual, velocity pair
+    (+ prediction)."""
+    return 14 + 8 * (p.mx * p.my * p.mz + p.mx * p.my) + (4 if with_prediction else 0)
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+def ncu_traffic():
+    """dram bytes per launch of the frame kernel from the committed ncu
+    capture (profiles/ncu_traffic.json), or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        if d.get("width") == WIDTH and d.get("height") == HEIGHT:
+            return float(d["dram_bytes_per_launch"])
+    except Exception:
+        pass
+    return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                 "-lms", "50", "-i", str(self.device)],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        try:
+            with open(self.path) as fh:
+                for line in fh:
+                    parts = [x.strip() for x in line.split(",")]
+                    if len(parts) >= 9 and parts[1].replace(".", "").isdigit():
+                        rows.append(parts)
+        except Exception:
+            pass
+        finally:
+            if self.path and os.path.exists(self.path):
+                os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no-samples"], "samples": 0}
+        sm = [float(r[1]) for r in rows]
+        load = [float(r[1]) for r in rows if float(r[3]) > 250.0] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(load)), "sm_max_mhz": float(rows[0][2]),
+                "reasons": reasons, "samples": len(rows), "power_w_max": max(float(r[3]) for r in rows)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_oracle_rate(params, frames_np, budget_s=12.0, threads=None, max_frames=64):
+    """Time the float64 oracle (the reference algorithm) on host cores.
+    frames_np: (T, H, W) float32 host frames.  Returns (rate, meta)."""
+    from oracle.oracle import OraclePipeline
+
+    threads = threads or os.cpu_count() or 1
+    t, h, w = frames_np.shape
+    with OraclePipeline(params, w, h, threads=threads) as orc:
+        n = 0
+        for n in range(params.mz + 1):  # warm-up + one untimed ready frame
+            orc.process_frame(frames_np[n % t])
+        done, spent = 0, 0.0
+        k = params.mz + 1
+        while (spent < budget_s or done < 2) and done < max_frames:
+            t0 = time.perf_counter()
+            orc.process_frame(frames_np[k % t])
+            spent += time.perf_counter() - t0
+            done += 1
+            k += 1
+    rate = done * h * w / spent
+    return rate, {"cores": threads, "frames": done, "seconds": spent, "height": h, "width": w}
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm (float64 oracle, bit-exact to
+    the reference package) on all host cores, same config/metric."""
+    world, rank, _ = dist_setup()
+    if rank != 0:
+        return
+    from paper_1408_3526_b200 import default_params
+    from paper_1408_3526_b200.scenegen import SimConfig, generate
+    from oracle.oracle import OraclePipeline
+
+    p = default_params()
+    threads = os.cpu_count() or 1
+    # bounded sample: size the crop height so the whole run fits ~150 s
+    probe_h = 64
+    frames, _ = generate(SimConfig(width=WIDTH, height=probe_h, frame_count=8, rng_seed=0))
+    with OraclePipeline(p, WIDTH, probe_h, threads=threads) as orc:
+        for f in frames[:6]:
+            orc.process_frame(f)
+        t0 = time.perf_counter()
+        orc.process_frame(frames[6])
+        per_row = (time.perf_counter() - t0) / probe_h
+    total = args.steps + args.warmup + p.mz
+    rows = int(min(HEIGHT, max(16, 150.0 / max(total, 1) / max(per_row, 1e-9))))
+    n_frames = min(total, 64)
+    frames, _ = generate(SimConfig(width=WIDTH, height=rows, frame_count=max(n_frames, 5), rng_seed=0))
+    with OraclePipeline(p, WIDTH, rows, threads=threads) as orc:
+        for k in range(p.mz - 1 + args.warmup):
+            orc.process_frame(frames[k % len(frames)])
+        t0 = time.perf_counter()
+        for k in range(args.steps):
+            orc.process_frame(frames[(p.mz - 1 + args.warmup + k) % len(frames)])
+        dt = time.perf_counter() - t0
+    value = args.steps * rows * WIDTH / dt
+    sample = (f"{args.steps} steady-state frames of a 640x{rows} crop of the C3 scene "
+              f"(float64 C oracle = reference algorithm, {threads} threads)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference scene generator)",
+        "config": {"workload": f"C3 640x{rows} crop, full pipeline, default FilterParams", "frame": [WIDTH, rows]},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import ctypes
+
+    import torch
+
+    from paper_1408_3526_b200 import Pipeline, _native, default_params
+    from paper_1408_3526_b200.scenegen import SimConfig, generate_device
+
+    world, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    p = default_params()
+    lib = _native.load()
+
+    n_frames = int(min(max(args.steps + args.warmup + p.mz, 64), 1000))
+    frames = generate_device(SimConfig(width=WIDTH, height=HEIGHT, frame_count=1000, rng_seed=rank),
+                             device=dev, frames=n_frames)
+    torch.cuda.synchronize()
+    # a dedicated (non-default) stream: the kernels, the frame copies and the
+    # timing events all live on it (stream handle 0 would mean "the
+    # pipeline's own stream" at the C ABI)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+    sh = ctypes.c_void_p(stream.cuda_stream)
+    assert sh.value, "expected a non-default CUDA stream"
+
+    pipe = Pipeline(p, WIDTH, HEIGHT, device=local)
+    h = pipe._h
+    ready, fidx = ctypes.c_int32(), ctypes.c_int64()
+
+    def push(k):
+        rc = lib.cw_push_device(h, ctypes.c_void_p(frames[k % n_frames].data_ptr()),
+                                ctypes.byref(ready), ctypes.byref(fidx), sh)
+        if rc:
+            _native.check(rc, h)
+
+    k = 0
+    for _ in range(p.mz - 1 + args.warmup):  # fill the temporal window, then warm up
+        push(k)
+        k += 1
+    torch.cuda.synchronize()
+    assert ready.value == 1
+    lib.cw_set_timing(h, 1)
+    ms_tot, launches = ctypes.c_double(), ctypes.c_int64()
+    lib.cw_kernel_time(h, ctypes.byref(ms_tot), ctypes.byref(launches))  # reset
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            push(k)
+            k += 1
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    elapsed_ms = ev0.elapsed_time(ev1)
+    lib.cw_kernel_time(h, ctypes.byref(ms_tot), ctypes.byref(launches))
+    lib.cw_set_timing(h, 0)
+    kern_ms = ms_tot.value / max(1, launches.value)
+    info = pipe.launch_info()
+    pipe.close()
+
+    # ---- e2e through the public API: pinned host frames, host outputs ----
+    from paper_1408_3526_b200 import Pipeline as PublicPipeline
+
+    e2e_steps = args.steps
+    n_host = min(n_frames, 256)
+    host = torch.empty((n_host, HEIGHT, WIDTH), dtype=torch.float32, pin_memory=True)
+    host.copy_(frames[:n_host])
+    host_np = host.numpy()
+    with PublicPipeline(p, WIDTH, HEIGHT, device=local) as pub:
+        j = 0
+        for _ in range(p.mz - 1 + args.warmup):
+            pub.process_frame(host_np[j % n_host])
+            j += 1
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            out = pub.process_frame(host_np[j % n_host])
+            j += 1
+        e2e_s = time.perf_counter() - t0
+    assert out is not None
+    h2d = WIDTH * HEIGHT * 4
+    d2h = WIDTH * HEIGHT * (4 + 4 + 2)
+
+    t = torch.tensor([elapsed_ms, e2e_s], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed_ms, e2e_s = float(t[0]), float(t[1])
+    px = WIDTH * HEIGHT
+    value = world * px * args.steps / (elapsed_ms / 1e3)
+    e2e = world * px * e2e_steps / e2e_s
+
+    peak, peak_kind = measured_peak()
+    bpp = b_alg(p, with_prediction=True)
+    achieved = bpp * px / (kern_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": ncu_traffic(),
+                "peak_kind": peak_kind, "bytes_per_px_frame": bpp,
+                "kernel_ms": kern_ms, "launches_timed": int(launches.value)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        host_frames = frames[: min(n_frames, 16)].cpu().numpy()
+        rate, meta = cpu_oracle_rate(p, host_frames, budget_s=args.cpu_budget)
+        cpu = {"value": rate, "unit": UNIT, "cores": meta["cores"], "kind": "port",
+               "sample": (f"{meta['frames']} steady-state 640x512 C3 frames in {meta['seconds']:.1f}s, "
+                          "float64 C oracle (reference algorithm, bit-exact to clutterwhiten)")}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (reference scene model: 25 drifting cosines + target + noise, generated on device)",
+            "config": {"workload": "C3: 640x512 frames, full SDFT->deadbeat->autocorr->PEF chain, default FilterParams",
+                       "frame": [WIDTH, HEIGHT], "streams": world,
+                       "parallelism": "independent stream per GPU" if world > 1 else "single GPU",
+                       "l2": "state 0.5 GB/stream >> 126 MB L2 (no flush needed)",
+                       "grid": info["grid"], "block": info["block"], "smem_bytes": info["smem_bytes"]},
+            "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "api": "Pipeline.process_frame (pinned host frame in, host residual/prediction/velocity out)"},
+            "gpu_launches": int(args.steps * info["kernels_per_push"]),
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU-oracle timing")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -124,6 +124,13 @@ int cw_read_view(cw_handle *h, int32_t what, void *dst, size_t bytes);
 int cw_launch_info(const cw_handle *h, int32_t *kernels_per_push, int32_t *grid, int32_t *block,
                    int32_t *smem_bytes);
 
+/* Per-launch device timing of the frame kernel: when on, every push
+ * records a CUDA event pair around the kernel on the launch stream;
+ * cw_kernel_time returns the summed kernel milliseconds and the number
+ * of launches since the last call (and resets the record). */
+int cw_set_timing(cw_handle *h, int32_t on);
+int cw_kernel_time(cw_handle *h, double *total_ms, int64_t *launches);
+
 /* Library/ABI identification. */
 int32_t cw_abi_version(void);
 

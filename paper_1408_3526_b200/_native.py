@@ -17,7 +17,7 @@ from .params import ParamError
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_PKG)
-LIB_PATH = os.path.join(_PKG, "libcw_b200.so")
+LIB_PATH = os.environ.get("CW_B200_LIB") or os.path.join(_PKG, "libcw_b200.so")
 CSRC = os.path.join(_PKG, "csrc")
 
 NVCC_FLAGS = [
@@ -32,7 +32,8 @@ CW_OK, CW_ERR_PARAM, CW_ERR_VALUE, CW_ERR_CUDA, CW_ERR_NOMEM, CW_ERR_UNSUPPORTED
 EXPORTS = (
     "cw_abi_version", "cw_create", "cw_destroy", "cw_last_error", "cw_set_forced_velocity",
     "cw_push", "cw_push_device", "cw_device_outputs", "cw_next_frame_slot", "cw_push_inplace",
-    "cw_frames_seen", "cw_set_debug", "cw_read_view", "cw_launch_info",
+    "cw_frames_seen", "cw_set_debug", "cw_read_view", "cw_launch_info", "cw_set_timing",
+    "cw_kernel_time",
 )
 
 
@@ -96,6 +97,8 @@ def load():
         "cw_set_debug": (ctypes.c_int, [vp, i32]),
         "cw_read_view": (ctypes.c_int, [vp, i32, vp, ctypes.c_size_t]),
         "cw_launch_info": (ctypes.c_int, [vp, P(i32), P(i32), P(i32), P(i32)]),
+        "cw_set_timing": (ctypes.c_int, [vp, i32]),
+        "cw_kernel_time": (ctypes.c_int, [vp, P(ctypes.c_double), P(i64)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

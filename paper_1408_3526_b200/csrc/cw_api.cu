@@ -91,6 +91,10 @@ struct cw_handle {
     bool have_that = false;
     bool debug = false;
     int forced_ix = -1, forced_iy = -1;
+    // optional per-launch timing: events recorded around each frame kernel
+    bool timing = false;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
     std::string err;
 };
 
@@ -169,12 +173,16 @@ static void build_tables(cw_handle *h)
         t.twc[k] = (float)std::cos(2 * PI * k / My);
         t.tws[k] = (float)std::sin(2 * PI * k / My);
     }
+    // S = norm * z+; the three unscaled Hann passes each scale by 4, so
+    // P = |C|^2 = norm^2 / 4^6 |C_unscaled|^2: fold into the kz collapse.
+    const double norm = 1.0 / std::sqrt((double)Mx * My * Mz);
+    const double pscale = norm * norm / 4096.0;
     for (int i = 0; i < Mz; i++) {
         const int kz = i - h->kz;
         t.wc[i] = (float)std::cos(2 * PI * kz / Mz);
         t.ws[i] = (float)std::sin(2 * PI * kz / Mz);
-        t.azc[i] = (float)std::cos(2 * PI * kz / Mz);
-        t.azs[i] = (float)-std::sin(2 * PI * kz / Mz);
+        t.azc[i] = (float)(pscale * std::cos(2 * PI * kz / Mz));
+        t.azs[i] = (float)(-pscale * std::sin(2 * PI * kz / Mz));
     }
     std::vector<double> gx(h->nlx), gy(h->nly);
     for (int i = 0; i < h->nlx; i++)
@@ -222,8 +230,20 @@ static void build_tables(cw_handle *h)
         t.rix[rk] = (uint8_t)(i % h->nlx);
         t.riy[rk] = (uint8_t)(i / h->nlx);
     }
-    t.cS = (float)(Mz / std::sqrt((double)Mx * My * Mz));
+    t.norm = (float)norm;
     t.inv_mz = (float)(1.0 / Mz);
+    // +-lag pairing needs an odd grid symmetric about an exact 0
+    auto symmetric = [](const std::vector<double> &g) {
+        const int n = (int)g.size();
+        if (n % 2 == 0 || g[n / 2] != 0.0)
+            return 0;
+        for (int i = 0; i < n / 2; i++)
+            if (g[i] != -g[n - 1 - i])
+                return 0;
+        return 1;
+    };
+    t.sym_x = symmetric(h->lag_x);
+    t.sym_y = symmetric(h->lag_y);
     t.alpha = (float)h->alpha;
     t.beta = (float)(1.0 - h->alpha);
     t.nlx = h->nlx;
@@ -232,8 +252,8 @@ static void build_tables(cw_handle *h)
 
 // PEF coefficients on the stored half space (pipeline.py:269-282,
 // _kernels.py:330-342): pred = Re sum_k c(k) S(k) over the retained band,
-// folded so that the kernel computes sum_j coef[j] * xhat+[j] with
-// S = cS * xhat+, pairing k with -k: Re(c S) + Re(c' conj S)
+// folded so that the kernel computes sum_j coef[j] * z+[j] with
+// S = norm * z+, pairing k with -k: Re(c S) + Re(c' conj S)
 //   = S.re (c.re + c'.re) + S.im (c'.im - c.im).
 static int build_coef(cw_handle *h, const float *bank, const int64_t *retained, int nret,
                       std::vector<float> *out)
@@ -249,7 +269,8 @@ static int build_coef(cw_handle *h, const float *bank, const int64_t *retained, 
         pos[retained[j]] = j;
     }
     auto flat = [&](int kz, int ky, int kx) { return ((kz + KZ) * My + (ky + KY)) * Mx + (kx + KX); };
-    const double cS = Mz / std::sqrt((double)Mx * My * Mz);
+    // the kernel holds z+ = Mz xhat+ (unnormalised DFT), S = norm * z+
+    const double cS = 1.0 / std::sqrt((double)Mx * My * Mz);
     const int NRET = Mz * WX * (2 * BY + 1);
     out->assign((size_t)h->nlx * h->nly * NRET, 0.f);
     for (int v = 0; v < h->nlx * h->nly; v++) {
@@ -414,6 +435,8 @@ void cw_destroy(cw_handle *h)
     cudaFree(h->d_pred);
     cudaFree(h->d_vidx);
     cudaFree(h->d_dbg);
+    for (cudaEvent_t e : h->ev_pool)
+        cudaEventDestroy(e);
     if (h->own)
         cudaStreamDestroy(h->own);
     delete h;
@@ -490,8 +513,22 @@ static int run_frame(cw_handle *h, cudaStream_t s, int32_t *ready, int64_t *fram
     a.forced_iy = h->forced_iy;
     a.mhx = h->mhx;
     a.mhy = h->mhy;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (h->timing) {
+        while (h->ev_pool.size() < h->ev_used + 2) {
+            cudaEvent_t e;
+            CW_CUDA(h, cudaEventCreate(&e));
+            h->ev_pool.push_back(e);
+        }
+        e0 = h->ev_pool[h->ev_used];
+        e1 = h->ev_pool[h->ev_used + 1];
+        h->ev_used += 2;
+        CW_CUDA(h, cudaEventRecord(e0, s));
+    }
     h->fn.launch(a, h->tab, h->grid, s);
     CW_CUDA(h, cudaGetLastError());
+    if (h->timing)
+        CW_CUDA(h, cudaEventRecord(e1, s));
     h->frames_seen = n + 1;
     if (rd)
         h->have_that = true;
@@ -584,6 +621,32 @@ int cw_launch_info(const cw_handle *h, int32_t *kernels_per_push, int32_t *grid,
         *block = h->fn.threads;
     if (smem_bytes)
         *smem_bytes = (int32_t)h->fn.smem;
+    return CW_OK;
+}
+
+int cw_set_timing(cw_handle *h, int32_t on)
+{
+    if (!h)
+        return CW_ERR_VALUE;
+    h->timing = on != 0;
+    h->ev_used = 0;
+    return CW_OK;
+}
+
+int cw_kernel_time(cw_handle *h, double *total_ms, int64_t *launches)
+{
+    if (!h || !total_ms || !launches)
+        return CW_ERR_VALUE;
+    double tot = 0.0;
+    for (size_t i = 0; i + 1 < h->ev_used; i += 2) {
+        CW_CUDA(h, cudaEventSynchronize(h->ev_pool[i + 1]));
+        float ms = 0.f;
+        CW_CUDA(h, cudaEventElapsedTime(&ms, h->ev_pool[i], h->ev_pool[i + 1]));
+        tot += ms;
+    }
+    *total_ms = tot;
+    *launches = (int64_t)(h->ev_used / 2);
+    h->ev_used = 0;
     return CW_OK;
 }
 

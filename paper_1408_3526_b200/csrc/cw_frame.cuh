@@ -30,7 +30,10 @@ namespace cwb {
 constexpr int MAXK = 5;    // largest half window supported by the tables
 constexpr int MAXM = 2 * MAXK + 1;
 constexpr int MAXL = 33;   // largest lag grid per axis
-constexpr int RESTART = 32;  // rows between direct y-SDFT restarts (bounds f32 drift)
+constexpr int RESTART = 32;
+#ifndef CW_MINB
+#define CW_MINB 2  // resident CTAs per SM the register budget is sized for
+#endif  // rows between direct y-SDFT restarts (bounds f32 drift)
 
 struct Tables {
     // x stage: cos/sin(2 pi kx m / Mx), kx = 0..KX, m = 0..Mx-1
@@ -41,7 +44,8 @@ struct Tables {
     float twc[MAXK + 1], tws[MAXK + 1];
     // observer rotation w(kz) = exp(+j 2 pi kz / Mz), index kz + KZ
     float wc[MAXM], ws[MAXM];
-    // kz collapse a_z(kz) = exp(-j 2 pi kz / Mz), index kz + KZ
+    // kz collapse a_z(kz) = exp(-j 2 pi kz / Mz), index kz + KZ, times
+    // norm^2 / 4096 (the three unscaled Hann passes each carry a factor 4)
     float azc[MAXM], azs[MAXM];
     // stage 1 (gx folded): B(ky,lx) = g*T(0) + sum_kx c*A - j s*D
     float s1g[MAXL], s1c[MAXL][MAXK], s1s[MAXL][MAXK];
@@ -50,10 +54,11 @@ struct Tables {
     // argmax total order: rank[ly * nlx + lx]; rank -> (ix, iy)
     uint16_t rank[MAXL * MAXL];
     uint8_t rix[MAXL * MAXL], riy[MAXL * MAXL];
-    float cS;      // Mz / sqrt(Mx My Mz): S = cS * xhat+
+    float norm;    // 1/sqrt(Mx My Mz): S = norm * z+ (z = Mz * xhat, unnormalised DFT)
     float inv_mz;  // observer gain 1/Mz
     float alpha, beta;
     int nlx, nly;
+    int sym_x, sym_y;  // lag grid symmetric about an exact 0 (odd length): +-l pairing
 };
 
 struct FrameArgs {
@@ -101,7 +106,8 @@ struct Geo {
     static constexpr int SM_RET = NRET * 32;
     static constexpr int SM_BEST = NR * 32 * 2;
     static constexpr int SM_PEF = (BY + 1) * 32;
-    static constexpr int SMEM_FLOATS = SM_XF + SM_CXBB + SM_RET + SM_BEST + SM_PEF;
+    static constexpr int SM_RANK = (MAXL * MAXL + 1) / 2;  // uint16 rank table
+    static constexpr int SMEM_FLOATS = SM_XF + SM_CXBB + SM_RET + SM_BEST + SM_PEF + SM_RANK;
     static constexpr size_t SMEM_BYTES = sizeof(float) * SMEM_FLOATS;
 };
 
@@ -113,10 +119,11 @@ __device__ __forceinline__ cf cadd(cf a, cf b) { return cf{a.r + b.r, a.i + b.i}
 __device__ __forceinline__ cf csub(cf a, cf b) { return cf{a.r - b.r, a.i - b.i}; }
 __device__ __forceinline__ cf cmul(cf a, cf b) { return cf{a.r * b.r - a.i * b.i, a.r * b.i + a.i * b.r}; }
 __device__ __forceinline__ cf cconj(cf a) { return cf{a.r, -a.i}; }
-// 1/2 c - 1/4 (a + b): one tap of the circular (-1/4, 1/2, -1/4) Hann
-__device__ __forceinline__ cf hann(cf a, cf c, cf b)
+// 2c - (a + b) = 4 x one tap of the circular (-1/4, 1/2, -1/4) Hann
+// (_kernels.py:177-217); the 4^3 is folded into the kz-collapse table.
+__device__ __forceinline__ cf hann4(cf a, cf c, cf b)
 {
-    return cf{fmaf(0.5f, c.r, -0.25f * (a.r + b.r)), fmaf(0.5f, c.i, -0.25f * (a.i + b.i))};
+    return cf{fmaf(2.f, c.r, -(a.r + b.r)), fmaf(2.f, c.i, -(a.i + b.i))};
 }
 
 // Total order of the reference pick (_kernels.py:286-298): larger score,
@@ -127,7 +134,7 @@ __device__ __forceinline__ bool better(float v, int rk, float best, int brk)
 }
 
 template <class G>
-__global__ void __launch_bounds__(G::NTHREADS, 2)
+__global__ void __launch_bounds__(G::NTHREADS, CW_MINB)
 cw_frame_kernel(const FrameArgs a, const Tables t)
 {
     constexpr int KX = G::KX, KY = G::KY, KZ = G::KZ, BX = G::BX, BY = G::BY;
@@ -135,27 +142,32 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
     constexpr int NR = G::NR, RING = G::RING;
 
     extern __shared__ float smem[];
-    float *xfr = smem;                      // [RING][XF][32]
-    float *cxb = xfr + G::SM_XF;            // [NR][MZ][MX][2][32]   (Hy exchange)
-    float *bb = cxb;                        // [NR][nlx][2][32]      (stage-1 exchange, aliased)
-    float *sret = cxb + G::SM_CXBB;         // [NRET][32]            (retained xhat+)
+    float *xfr = smem;                      // [RING][XF][32]       x-stage ring
+    float *cxb = xfr + G::SM_XF;            // [NR][MZ][MX][2][32]  Hy exchange
+    float *bb = cxb;                        // [NR][MAXL][2][32]    stage-1 exchange (aliased)
+    float *sret = cxb + G::SM_CXBB;         // [NRET][32]           retained z+
     float *pbest = sret + G::SM_RET;        // [NR][32] score
     int *prank = reinterpret_cast<int *>(pbest + NR * 32);  // [NR][32]
     float *ppef = pbest + G::SM_BEST;       // [BY+1][32]
+    uint16_t *srank = reinterpret_cast<uint16_t *>(ppef + G::SM_PEF);  // [nly][nlx]
 
     const int lane = threadIdx.x & 31;
     const int r = threadIdx.x >> 5;  // spatial-frequency row ky of this warp
     const int W = a.W, H = a.H, NXB = a.NXB;
+    const int nlx = t.nlx, nly = t.nly;
     const int rows = H - a.y_begin;
     const long long units = (long long)NXB * rows;
     const long long u0 = units * blockIdx.x / gridDim.x;
     const long long u1 = units * (blockIdx.x + 1) / gridDim.x;
 
+    for (int i = threadIdx.x; i < nlx * nly; i += G::NTHREADS) srank[i] = t.rank[i];
+
 #define XFR(slot, f) xfr[((slot) * G::XF + (f)) * 32 + lane]
 #define CXB(rr, kzi, kxi, c) cxb[((((rr) * MZ + (kzi)) * MX + (kxi)) * 2 + (c)) * 32 + lane]
+#define BB(rr, lx, c) bb[(((rr) * MAXL + (lx)) * 2 + (c)) * 32 + lane]
 
-    // x stage for local row yy at column x: 9-tap windowed sums (the row
-    // sweep), zero padding outside the frame.  kx = 0 real, kx > 0 complex.
+    // x stage for local row yy at column x: Mx-tap window sums (the row
+    // sweep, _kernels.py:31-45), zero outside the frame; kx = 0 real.
     auto xstage = [&](int yy, int x, int slot) {
         float acc[G::XF];
 #pragma unroll
@@ -178,11 +190,28 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
         for (int f = 0; f < G::XF; f++) XFR(slot, f) = acc[f];
     };
     auto ring_slot = [&](int yy) { return ((yy % RING) + RING) % RING; };
-    // x-stage value for bin kx (negative kx by conjugate symmetry)
     auto xfv = [&](int slot, int kx) -> cf {
         if (kx == 0) return cmk(XFR(slot, 0), 0.f);
         if (kx > 0) return cmk(XFR(slot, 2 * kx - 1), XFR(slot, 2 * kx));
         return cmk(XFR(slot, -2 * kx - 1), -XFR(slot, -2 * kx));
+    };
+    // this warp's observer floats and T^ floats of pixel row yy (registers)
+    const int nst = (r == 0) ? G::ROW0 : G::ROWN;
+    const int nth = (r == 0) ? G::TROW0 : G::TROWN;
+    float st[G::ROWN];
+    float thv[G::TROWN];
+    auto load_rows = [&](int yy, int xb, bool with_that) {
+        const size_t pix = (size_t)yy * NXB + xb;
+        const float *sp_ = a.state + (pix * G::NS + G::srow(r)) * 32 + lane;
+#pragma unroll
+        for (int j = 0; j < G::ROWN; j++)
+            if (j < nst) st[j] = sp_[j * 32];
+        if (with_that) {
+            const float *tp = a.that + (pix * G::NT + G::trow(r)) * 32 + lane;
+#pragma unroll
+            for (int j = 0; j < G::TROWN; j++)
+                if (j < nth) thv[j] = tp[j * 32];
+        }
     };
 
     long long u = u0;
@@ -194,24 +223,23 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
         const int x = xb * 32 + lane;
         const bool colv = x < W;
 
-        // prologue: x stage of rows ys-MY+1 .. ys (split over warps)
-        __syncthreads();
+        __syncthreads();  // ring reuse across chunks
         for (int k = r; k < MY; k += NR) {
             const int yy = ys - MY + 1 + k;
             xstage(yy, x, ring_slot(yy));
         }
+        load_rows(ys, xb, a.ready && !a.first);
         __syncthreads();
 
-        // y-SDFT resonator state of this warp's row, kx = -KX..KX
-        cf sp[MX];
+        cf sp[MX];  // y-SDFT resonators of row ky = r, kx = -KX..KX
 #pragma unroll
         for (int i = 0; i < MX; i++) sp[i] = cmk(0.f, 0.f);
 
         for (int yy = ys; yy < ye; yy++) {
-            // ---------------- phase B: spatial, observer, Hz, Hx ----------------
+            // ---------------- phase B: spatial SDFT, observer, Hz, Hx ----------------
             if (r == 0 && yy + 1 < ye) xstage(yy + 1, x, ring_slot(yy + 1));
             if (((yy - ys) % RESTART) == 0) {
-                // direct restart: sp = sum_my e^{+j 2 pi ky my / My} xf(yy - my)
+                // direct restart sum_my e^{+j 2 pi ky my / My} xf(yy - my) (_kernels.py:58-61)
 #pragma unroll
                 for (int i = 0; i < MX; i++) sp[i] = cmk(0.f, 0.f);
                 for (int m = 0; m < MY; m++) {
@@ -221,6 +249,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                     for (int i = 0; i < MX; i++) sp[i] = cadd(sp[i], cmul(e, xfv(sl, i - KX)));
                 }
             } else {
+                // comb + resonator (_kernels.py:62-68)
                 const int s1 = ring_slot(yy), s0 = ring_slot(yy - MY);
                 const cf tw = cmk(t.twc[r], t.tws[r]);
 #pragma unroll
@@ -228,38 +257,36 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
             }
             const bool anchor = colv && x >= MX - 1 && (yy + a.y_off) >= MY - 1;
             const size_t pix = (size_t)yy * NXB + xb;
-            float *st = a.state + pix * G::NS * 32 + lane;
-            float *dbg = a.dbgS ? a.dbgS + pix * G::NS * 32 + lane : nullptr;
+            float *stg = a.state + (pix * G::NS + G::srow(r)) * 32 + lane;
+            float *dbg = a.dbgS ? a.dbgS + (pix * G::NS + G::srow(r)) * 32 + lane : nullptr;
 
-            // observer + Hz: cz[kxi][kzi] (kxi = kx + KX); row 0 uses kx >= 0 only
-            cf cz[MX][MZ];
+            // Deadbeat observer on z = Mz * xhat (state in HBM, in place):
+            //   e = u - (1/Mz) sum_kz z ;  z+ = z + e ;  z <- w(kz) z+
+            // z+ is exactly the reference's unnormalised temporal DFT of the
+            // last Mz spatial spectra (_kernels.py:71-90, S = norm * z+).
+            cf cz[MX][MZ];  // 4 x Hz(z+) per kx column
             if (r == 0) {
-                // DC spatial bin: real input, states kz = 0 (real) and kz = 1..KZ
-                {
-                    const float u0v = anchor ? sp[KX].r : 0.f;
-                    float s0 = st[0];
-                    cf s[KZ + 1];
+                {   // DC spatial bin: real input; z(0) real, z(1..KZ) complex
+                    const float uv = anchor ? sp[KX].r : 0.f;
+                    float sum = st[0];
 #pragma unroll
-                    for (int kz = 1; kz <= KZ; kz++) s[kz] = cmk(st[(1 + 2 * (kz - 1)) * 32], st[(2 + 2 * (kz - 1)) * 32]);
-                    float sum = s0;
-#pragma unroll
-                    for (int kz = 1; kz <= KZ; kz++) sum += 2.f * s[kz].r;
-                    const float e = (u0v - sum) * t.inv_mz;
-                    const float xp0 = s0 + e;
-                    st[0] = xp0;
-                    if (BY >= 0) sret[0 * 32 + lane] = xp0;
-                    if (dbg) dbg[0] = t.cS * xp0;
+                    for (int kz = 1; kz <= KZ; kz++) sum = fmaf(2.f, st[2 * kz - 1], sum);
+                    const float e = fmaf(-t.inv_mz, sum, uv);
+                    const float z0 = st[0] + e;
+                    stg[0] = z0;
+                    sret[lane] = z0;
+                    if (dbg) dbg[0] = t.norm * z0;
 #pragma unroll
                     for (int kz = 1; kz <= KZ; kz++) {
-                        const cf xp = cmk(s[kz].r + e, s[kz].i);
-                        const cf xn = cmul(cmk(t.wc[kz + KZ], t.ws[kz + KZ]), xp);
-                        st[(1 + 2 * (kz - 1)) * 32] = xn.r;
-                        st[(2 + 2 * (kz - 1)) * 32] = xn.i;
-                        sret[(1 + 2 * (kz - 1)) * 32 + lane] = xp.r;
-                        sret[(2 + 2 * (kz - 1)) * 32 + lane] = xp.i;
+                        const cf zp = cmk(st[2 * kz - 1] + e, st[2 * kz]);
+                        const cf zn = cmul(cmk(t.wc[kz + KZ], t.ws[kz + KZ]), zp);
+                        stg[(2 * kz - 1) * 32] = zn.r;
+                        stg[(2 * kz) * 32] = zn.i;
+                        sret[(2 * kz - 1) * 32 + lane] = zp.r;
+                        sret[(2 * kz) * 32 + lane] = zp.i;
                         if (dbg) {
-                            dbg[(1 + 2 * (kz - 1)) * 32] = t.cS * xp.r;
-                            dbg[(2 + 2 * (kz - 1)) * 32] = t.cS * xp.i;
+                            dbg[(2 * kz - 1) * 32] = t.norm * zp.r;
+                            dbg[(2 * kz) * 32] = t.norm * zp.i;
                         }
                     }
                 }
@@ -270,36 +297,29 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                 for (int kx = 1; kx <= KX; kx++) {
                     const int base = MZ + (kx - 1) * 2 * MZ;
                     const cf uv = anchor ? sp[KX + kx] : cmk(0.f, 0.f);
-                    cf s[MZ];
                     cf sum = cmk(0.f, 0.f);
 #pragma unroll
-                    for (int kzi = 0; kzi < MZ; kzi++) {
-                        s[kzi] = cmk(st[(base + 2 * kzi) * 32], st[(base + 2 * kzi + 1) * 32]);
-                        sum = cadd(sum, s[kzi]);
-                    }
-                    const cf e = cmk((uv.r - sum.r) * t.inv_mz, (uv.i - sum.i) * t.inv_mz);
-                    cf xp[MZ];
+                    for (int kzi = 0; kzi < MZ; kzi++) sum = cadd(sum, cmk(st[base + 2 * kzi], st[base + 2 * kzi + 1]));
+                    const cf e = cmk(fmaf(-t.inv_mz, sum.r, uv.r), fmaf(-t.inv_mz, sum.i, uv.i));
+                    cf zp[MZ];
 #pragma unroll
                     for (int kzi = 0; kzi < MZ; kzi++) {
-                        xp[kzi] = cadd(s[kzi], e);
-                        const cf xn = cmul(cmk(t.wc[kzi], t.ws[kzi]), xp[kzi]);
-                        st[(base + 2 * kzi) * 32] = xn.r;
-                        st[(base + 2 * kzi + 1) * 32] = xn.i;
+                        zp[kzi] = cmk(st[base + 2 * kzi] + e.r, st[base + 2 * kzi + 1] + e.i);
+                        const cf zn = (kzi == KZ) ? zp[kzi] : cmul(cmk(t.wc[kzi], t.ws[kzi]), zp[kzi]);
+                        stg[(base + 2 * kzi) * 32] = zn.r;
+                        stg[(base + 2 * kzi + 1) * 32] = zn.i;
                         if (kx <= BX) {
-                            sret[(base + 2 * kzi) * 32 + lane] = xp[kzi].r;
-                            sret[(base + 2 * kzi + 1) * 32 + lane] = xp[kzi].i;
+                            sret[(base + 2 * kzi) * 32 + lane] = zp[kzi].r;
+                            sret[(base + 2 * kzi + 1) * 32 + lane] = zp[kzi].i;
                         }
                         if (dbg) {
-                            dbg[(base + 2 * kzi) * 32] = t.cS * xp[kzi].r;
-                            dbg[(base + 2 * kzi + 1) * 32] = t.cS * xp[kzi].i;
+                            dbg[(base + 2 * kzi) * 32] = t.norm * zp[kzi].r;
+                            dbg[(base + 2 * kzi + 1) * 32] = t.norm * zp[kzi].i;
                         }
                     }
-                    // Hz (temporal Hann, circular) scaled to the unitary spectrum
 #pragma unroll
-                    for (int kzi = 0; kzi < MZ; kzi++) {
-                        const cf h = hann(xp[(kzi + MZ - 1) % MZ], xp[kzi], xp[(kzi + 1) % MZ]);
-                        cz[KX + kx][kzi] = cmk(t.cS * h.r, t.cS * h.i);
-                    }
+                    for (int kzi = 0; kzi < MZ; kzi++)
+                        cz[KX + kx][kzi] = hann4(zp[(kzi + MZ - 1) % MZ], zp[kzi], zp[(kzi + 1) % MZ]);
                 }
                 // kx < 0 by symmetry: C(kz, 0, -kx) = conj C(-kz, 0, kx)
 #pragma unroll
@@ -307,43 +327,35 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
 #pragma unroll
                     for (int kzi = 0; kzi < MZ; kzi++) cz[KX - kx][kzi] = cconj(cz[KX + kx][MZ - 1 - kzi]);
             } else {
-                float *sr = st + G::srow(r) * 32;
-                float *dr = dbg ? dbg + G::srow(r) * 32 : nullptr;
-                float *rr = sret + (G::prow(r < BY + 1 ? r : 0) * 32) + lane;
+                float *rr = sret + G::prow(r <= BY ? r : 0) * 32 + lane;
 #pragma unroll
                 for (int kxi = 0; kxi < MX; kxi++) {
                     const int base = kxi * MZ * 2;
                     const cf uv = anchor ? sp[kxi] : cmk(0.f, 0.f);
-                    cf s[MZ];
                     cf sum = cmk(0.f, 0.f);
 #pragma unroll
-                    for (int kzi = 0; kzi < MZ; kzi++) {
-                        s[kzi] = cmk(sr[(base + 2 * kzi) * 32], sr[(base + 2 * kzi + 1) * 32]);
-                        sum = cadd(sum, s[kzi]);
-                    }
-                    const cf e = cmk((uv.r - sum.r) * t.inv_mz, (uv.i - sum.i) * t.inv_mz);
-                    cf xp[MZ];
+                    for (int kzi = 0; kzi < MZ; kzi++) sum = cadd(sum, cmk(st[base + 2 * kzi], st[base + 2 * kzi + 1]));
+                    const cf e = cmk(fmaf(-t.inv_mz, sum.r, uv.r), fmaf(-t.inv_mz, sum.i, uv.i));
+                    cf zp[MZ];
                     const int kxb = kxi - KX + BX;  // retained-band column
 #pragma unroll
                     for (int kzi = 0; kzi < MZ; kzi++) {
-                        xp[kzi] = cadd(s[kzi], e);
-                        const cf xn = cmul(cmk(t.wc[kzi], t.ws[kzi]), xp[kzi]);
-                        sr[(base + 2 * kzi) * 32] = xn.r;
-                        sr[(base + 2 * kzi + 1) * 32] = xn.i;
+                        zp[kzi] = cmk(st[base + 2 * kzi] + e.r, st[base + 2 * kzi + 1] + e.i);
+                        const cf zn = (kzi == KZ) ? zp[kzi] : cmul(cmk(t.wc[kzi], t.ws[kzi]), zp[kzi]);
+                        stg[(base + 2 * kzi) * 32] = zn.r;
+                        stg[(base + 2 * kzi + 1) * 32] = zn.i;
                         if (r <= BY && kxb >= 0 && kxb < G::WX) {
-                            rr[((kxb * MZ + kzi) * 2) * 32] = xp[kzi].r;
-                            rr[((kxb * MZ + kzi) * 2 + 1) * 32] = xp[kzi].i;
+                            rr[((kxb * MZ + kzi) * 2) * 32] = zp[kzi].r;
+                            rr[((kxb * MZ + kzi) * 2 + 1) * 32] = zp[kzi].i;
                         }
-                        if (dr) {
-                            dr[(base + 2 * kzi) * 32] = t.cS * xp[kzi].r;
-                            dr[(base + 2 * kzi + 1) * 32] = t.cS * xp[kzi].i;
+                        if (dbg) {
+                            dbg[(base + 2 * kzi) * 32] = t.norm * zp[kzi].r;
+                            dbg[(base + 2 * kzi + 1) * 32] = t.norm * zp[kzi].i;
                         }
                     }
 #pragma unroll
-                    for (int kzi = 0; kzi < MZ; kzi++) {
-                        const cf h = hann(xp[(kzi + MZ - 1) % MZ], xp[kzi], xp[(kzi + 1) % MZ]);
-                        cz[kxi][kzi] = cmk(t.cS * h.r, t.cS * h.i);
-                    }
+                    for (int kzi = 0; kzi < MZ; kzi++)
+                        cz[kxi][kzi] = hann4(zp[(kzi + MZ - 1) % MZ], zp[kzi], zp[(kzi + 1) % MZ]);
                 }
             }
             if (a.ready) {
@@ -352,17 +364,16 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                 for (int kzi = 0; kzi < MZ; kzi++)
 #pragma unroll
                     for (int kxi = 0; kxi < MX; kxi++) {
-                        const cf h = hann(cz[(kxi + MX - 1) % MX][kzi], cz[kxi][kzi], cz[(kxi + 1) % MX][kzi]);
+                        const cf h = hann4(cz[(kxi + MX - 1) % MX][kzi], cz[kxi][kzi], cz[(kxi + 1) % MX][kzi]);
                         CXB(r, kzi, kxi, 0) = h.r;
                         CXB(r, kzi, kxi, 1) = h.i;
                     }
             }
             __syncthreads();  // (1) Cx rows visible; x stage of yy+1 done
-            if (!a.ready) continue;
 
             // ---------------- phase C1: Hy, power, kz collapse, smoothing ----------------
             cf T[MX];
-            {
+            if (a.ready) {
                 const int klo = (r == 0) ? KX : 0;  // row 0: kx >= 0 only
 #pragma unroll
                 for (int kxi = 0; kxi < MX; kxi++) {
@@ -372,37 +383,34 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                     for (int kzi = 0; kzi < MZ; kzi++) {
                         const cf own = cmk(CXB(r, kzi, kxi, 0), CXB(r, kzi, kxi, 1));
                         cf up, dn;
-                        if (r == 0) {
+                        if (r == 0) {  // row -1 = conj-flip of row 1
                             up = cmk(CXB(1, MZ - 1 - kzi, MX - 1 - kxi, 0), -CXB(1, MZ - 1 - kzi, MX - 1 - kxi, 1));
                             dn = cmk(CXB(1, kzi, kxi, 0), CXB(1, kzi, kxi, 1));
                         } else {
                             up = cmk(CXB(r - 1, kzi, kxi, 0), CXB(r - 1, kzi, kxi, 1));
                             if (r < KY)
                                 dn = cmk(CXB(r + 1, kzi, kxi, 0), CXB(r + 1, kzi, kxi, 1));
-                            else
+                            else  // row KY+1 == -KY = conj-flip of row KY
                                 dn = cmk(CXB(KY, MZ - 1 - kzi, MX - 1 - kxi, 0), -CXB(KY, MZ - 1 - kzi, MX - 1 - kxi, 1));
                         }
-                        const cf c = hann(up, own, dn);
+                        const cf c = hann4(up, own, dn);
                         const float p = fmaf(c.r, c.r, c.i * c.i);
                         T[kxi].r = fmaf(t.azc[kzi], p, T[kxi].r);
                         T[kxi].i = fmaf(t.azs[kzi], p, T[kxi].i);
                     }
                 }
-                // smoothing (_kernels.py:261-271; first ready frame copies)
-                const size_t pix = (size_t)yy * NXB + xb;
-                float *th = a.that + pix * G::NT * 32 + G::trow(r) * 32 + lane;
+                // smoothing of T^ (_kernels.py:261-271; first ready frame copies)
+                float *th = a.that + (pix * G::NT + G::trow(r)) * 32 + lane;
                 if (r == 0) {
-                    // T(0,0) real, then kx = 1..KX complex
                     float v = T[KX].r;
-                    if (!a.first) v = fmaf(t.beta, v, t.alpha * th[0]);
+                    if (!a.first) v = fmaf(t.beta, v, t.alpha * thv[0]);
                     th[0] = v;
                     T[KX] = cmk(v, 0.f);
 #pragma unroll
                     for (int kx = 1; kx <= KX; kx++) {
                         cf v2 = T[KX + kx];
                         if (!a.first)
-                            v2 = cmk(fmaf(t.beta, v2.r, t.alpha * th[(2 * kx - 1) * 32]),
-                                     fmaf(t.beta, v2.i, t.alpha * th[(2 * kx) * 32]));
+                            v2 = cmk(fmaf(t.beta, v2.r, t.alpha * thv[2 * kx - 1]), fmaf(t.beta, v2.i, t.alpha * thv[2 * kx]));
                         th[(2 * kx - 1) * 32] = v2.r;
                         th[(2 * kx) * 32] = v2.i;
                         T[KX + kx] = v2;
@@ -412,19 +420,61 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                     for (int kxi = 0; kxi < MX; kxi++) {
                         cf v2 = T[kxi];
                         if (!a.first)
-                            v2 = cmk(fmaf(t.beta, v2.r, t.alpha * th[(2 * kxi) * 32]),
-                                     fmaf(t.beta, v2.i, t.alpha * th[(2 * kxi + 1) * 32]));
+                            v2 = cmk(fmaf(t.beta, v2.r, t.alpha * thv[2 * kxi]), fmaf(t.beta, v2.i, t.alpha * thv[2 * kxi + 1]));
                         th[(2 * kxi) * 32] = v2.r;
                         th[(2 * kxi + 1) * 32] = v2.i;
                         T[kxi] = v2;
                     }
                 }
             }
-            __syncthreads();  // (2) all Hy reads of cxb done before bb overwrites it
+            // prefetch the next row's observer and T^ rows (consumed after the
+            // remaining phases: hides the HBM latency behind them)
+            if (yy + 1 < ye) load_rows(yy + 1, xb, a.ready && !a.first);
+            if (!a.ready) continue;
+            __syncthreads();  // (2) Hy reads of cxb done before bb overwrites it
 
             // ---------------- phase C2: stage-1 lag contraction along kx ----------------
-            {
-                const int nlx = t.nlx;
+            // B(ky, lx) = gx(lx) sum_kx e^{-j 2 pi kx lx / Mx} T^(ky, kx)
+            if (t.sym_x) {
+                const int c0 = nlx >> 1;  // lag 0; lags +-p at c0 +- p
+                if (r == 0) {
+                    for (int q = 0; q <= c0; q++) {
+                        const int lx = c0 + q;
+                        float cp = t.s1g[lx] * T[KX].r, sp2 = 0.f;
+#pragma unroll
+                        for (int kx = 1; kx <= KX; kx++) {
+                            cp = fmaf(2.f * t.s1c[lx][kx - 1], T[KX + kx].r, cp);
+                            sp2 = fmaf(2.f * t.s1s[lx][kx - 1], T[KX + kx].i, sp2);
+                        }
+                        BB(0, c0 + q, 0) = cp + sp2;
+                        BB(0, c0 - q, 0) = cp - sp2;
+                    }
+                } else {
+                    cf A[KX + 1], D[KX + 1];
+#pragma unroll
+                    for (int kx = 1; kx <= KX; kx++) {
+                        A[kx] = cadd(T[KX + kx], T[KX - kx]);
+                        D[kx] = csub(T[KX + kx], T[KX - kx]);
+                    }
+                    for (int q = 0; q <= c0; q++) {
+                        const int lx = c0 + q;
+                        const float g = t.s1g[lx];
+                        float cr = g * T[KX].r, ci = g * T[KX].i, sr = 0.f, si = 0.f;
+#pragma unroll
+                        for (int kx = 1; kx <= KX; kx++) {
+                            const float c = t.s1c[lx][kx - 1], s = t.s1s[lx][kx - 1];
+                            cr = fmaf(c, A[kx].r, cr);
+                            ci = fmaf(c, A[kx].i, ci);
+                            sr = fmaf(s, D[kx].i, sr);
+                            si = fmaf(-s, D[kx].r, si);
+                        }
+                        BB(r, c0 + q, 0) = cr + sr;
+                        BB(r, c0 + q, 1) = ci + si;
+                        BB(r, c0 - q, 0) = cr - sr;
+                        BB(r, c0 - q, 1) = ci - si;
+                    }
+                }
+            } else {
                 if (r == 0) {
                     for (int lx = 0; lx < nlx; lx++) {
                         float b = t.s1g[lx] * T[KX].r;
@@ -433,7 +483,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                             b = fmaf(2.f * t.s1c[lx][kx - 1], T[KX + kx].r, b);
                             b = fmaf(2.f * t.s1s[lx][kx - 1], T[KX + kx].i, b);
                         }
-                        bb[((0 * MAXL + lx) * 2) * 32 + lane] = b;
+                        BB(0, lx, 0) = b;
                     }
                 } else {
                     cf A[KX + 1], D[KX + 1];
@@ -451,37 +501,59 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                             br = fmaf(c, A[kx].r, fmaf(s, D[kx].i, br));
                             bi = fmaf(c, A[kx].i, fmaf(-s, D[kx].r, bi));
                         }
-                        bb[((r * MAXL + lx) * 2) * 32 + lane] = br;
-                        bb[((r * MAXL + lx) * 2 + 1) * 32 + lane] = bi;
+                        BB(r, lx, 0) = br;
+                        BB(r, lx, 1) = bi;
                     }
                 }
             }
             __syncthreads();  // (3) B(ky, lx) visible
 
             // ---------------- phase D: stage-2 contraction along ky + partial argmax ----------------
+            // score(ly, lx) = gy gx R^(ly, lx) = s2g B0 + sum_ky s2c Re B + s2s Im B
             {
-                const int nlx = t.nlx, nly = t.nly;
                 float best = -INFINITY;
                 int brk = 0x7fffffff;
                 for (int lx = r; lx < nlx; lx += NR) {
-                    const float b0 = bb[((0 * MAXL + lx) * 2) * 32 + lane];
+                    const float b0 = BB(0, lx, 0);
                     float br[KY + 1], bi[KY + 1];
 #pragma unroll
                     for (int k = 1; k <= KY; k++) {
-                        br[k] = bb[((k * MAXL + lx) * 2) * 32 + lane];
-                        bi[k] = bb[((k * MAXL + lx) * 2 + 1) * 32 + lane];
+                        br[k] = BB(k, lx, 0);
+                        bi[k] = BB(k, lx, 1);
                     }
-                    for (int ly = 0; ly < nly; ly++) {
-                        float v = t.s2g[ly] * b0;
+                    if (t.sym_y) {
+                        // visit ly = 0, -1, +1, -2, +2, ...: ascending rank order within
+                        // a column (|v|^2 grows with |ly|, then iy ascending), so a
+                        // strict '>' keeps the reference's tie winner (_kernels.py:286-298)
+                        const int c0 = nly >> 1;
+                        float cb = t.s2g[c0] * b0;
 #pragma unroll
-                        for (int k = 1; k <= KY; k++) {
-                            v = fmaf(t.s2c[ly][k - 1], br[k], v);
-                            v = fmaf(t.s2s[ly][k - 1], bi[k], v);
+                        for (int k = 1; k <= KY; k++) cb = fmaf(t.s2c[c0][k - 1], br[k], cb);
+                        int ci = c0;
+                        for (int q = 1; q <= c0; q++) {
+                            const int ly = c0 + q;
+                            float e = t.s2g[ly] * b0, o = 0.f;
+#pragma unroll
+                            for (int k = 1; k <= KY; k++) {
+                                e = fmaf(t.s2c[ly][k - 1], br[k], e);
+                                o = fmaf(t.s2s[ly][k - 1], bi[k], o);
+                            }
+                            const float vm = e - o, vp = e + o;
+                            if (vm > cb) { cb = vm; ci = c0 - q; }
+                            if (vp > cb) { cb = vp; ci = ly; }
                         }
-                        const int rk = t.rank[ly * nlx + lx];
-                        if (better(v, rk, best, brk)) {
-                            best = v;
-                            brk = rk;
+                        const int rk = srank[ci * nlx + lx];
+                        if (better(cb, rk, best, brk)) { best = cb; brk = rk; }
+                    } else {
+                        for (int ly = 0; ly < nly; ly++) {
+                            float v = t.s2g[ly] * b0;
+#pragma unroll
+                            for (int k = 1; k <= KY; k++) {
+                                v = fmaf(t.s2c[ly][k - 1], br[k], v);
+                                v = fmaf(t.s2s[ly][k - 1], bi[k], v);
+                            }
+                            const int rk = srank[ly * nlx + lx];
+                            if (better(v, rk, best, brk)) { best = v; brk = rk; }
                         }
                     }
                 }
@@ -499,10 +571,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                 for (int w = 1; w < NR; w++) {
                     const float v = pbest[w * 32 + lane];
                     const int rk = prank[w * 32 + lane];
-                    if (better(v, rk, best, brk)) {
-                        best = v;
-                        brk = rk;
-                    }
+                    if (better(v, rk, best, brk)) { best = v; brk = rk; }
                 }
                 if (a.forced_ix >= 0) {
                     vix = a.forced_ix;
@@ -513,13 +582,18 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                 }
             }
             if (r <= BY) {
-                const float *cp = a.coefP + (size_t)(viy * t.nlx + vix) * G::NRET + G::prow(r);
+                // PEF on the retained band (_kernels.py:330-342), folded to the
+                // stored half space: pred = sum_j coef[v][j] * z+[j]
+                const float *cp = a.coefP + (size_t)(viy * nlx + vix) * G::NRET + G::prow(r);
                 const float *sr = sret + G::prow(r) * 32 + lane;
                 const int n = (r == 0) ? G::PROW0 : G::PROWN;
-                float acc = 0.f;
-#pragma unroll 5
-                for (int j = 0; j < n; j++) acc = fmaf(__ldg(cp + j), sr[j * 32], acc);
-                ppef[r * 32 + lane] = acc;
+                float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll 10
+                for (int j = 0; j < n; j += 2) {
+                    acc0 = fmaf(__ldg(cp + j), sr[j * 32], acc0);
+                    if (j + 1 < n) acc1 = fmaf(__ldg(cp + j + 1), sr[(j + 1) * 32], acc1);
+                }
+                ppef[r * 32 + lane] = acc0 + acc1;
             }
             if (r == 0 && colv) {
                 uint8_t *vp = a.vidx + ((size_t)yy * W + x) * 2;
@@ -541,6 +615,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
     }
 #undef XFR
 #undef CXB
+#undef BB
 }
 
 }  // namespace cwb
