@@ -27,45 +27,57 @@ struct LaunchFn {
     const void *kernel;
     int threads;
     size_t smem;
-    int ns, nt, nret;
+    int nsp, ntp, retp;  // float2 pairs per pixel: observer state, T^, retained
+    int nl;              // compiled lag count (0: runtime loops)
 };
 
-template <int KX, int KY, int KZ, int BX, int BY>
+template <int KX, int KY, int KZ, int BX, int BY, int NL>
 void launch_inst(const FrameArgs &a, const Tables &t, int grid, cudaStream_t s)
 {
     using G = Geo<KX, KY, KZ, BX, BY>;
-    cw_frame_kernel<G><<<grid, G::NTHREADS, G::SMEM_BYTES, s>>>(a, t);
+    cw_frame_kernel<G, NL><<<grid, G::NTHREADS, G::SMEM_BYTES, s>>>(a, t);
 }
 
-template <int KX, int KY, int KZ, int BX, int BY>
+template <int KX, int KY, int KZ, int BX, int BY, int NL>
 LaunchFn make_inst()
 {
     using G = Geo<KX, KY, KZ, BX, BY>;
     LaunchFn f;
-    f.launch = &launch_inst<KX, KY, KZ, BX, BY>;
-    f.kernel = reinterpret_cast<const void *>(&cw_frame_kernel<G>);
+    f.launch = &launch_inst<KX, KY, KZ, BX, BY, NL>;
+    f.kernel = reinterpret_cast<const void *>(&cw_frame_kernel<G, NL>);
     f.threads = G::NTHREADS;
     f.smem = G::SMEM_BYTES;
-    f.ns = G::NS;
-    f.nt = G::NT;
-    f.nret = G::NRET;
+    f.nsp = G::NSP;
+    f.ntp = G::NTP;
+    f.retp = G::RETP;
+    f.nl = NL;
     return f;
 }
 
 // Compiled geometries: the default (4,4,2,3,3) and the SURVEY §8d C5 sweep.
-bool find_inst(int kx, int ky, int kz, int bx, int by, LaunchFn *out)
+// Symmetric lag grids of 9/17/33 entries get fully unrolled contraction
+// kernels; any other grid runs the runtime-loop instance (NL = 0).
+bool find_inst(int kx, int ky, int kz, int bx, int by, int nl_sym, LaunchFn *out)
 {
-#define CW_INST(a, b, c, d, e)                                                  \
+#define CW_GEO(a, b, c, d, e, ...)                                              \
     if (kx == a && ky == b && kz == c && bx == d && by == e) {                 \
-        *out = make_inst<a, b, c, d, e>();                                      \
+        const int nls[] = {__VA_ARGS__};                                        \
+        (void)nls;                                                              \
+        CW_NL(a, b, c, d, e, 9) CW_NL(a, b, c, d, e, 17) CW_NL(a, b, c, d, e, 33) \
+        *out = make_inst<a, b, c, d, e, 0>();                                   \
         return true;                                                            \
     }
-    CW_INST(4, 4, 2, 3, 3)
-    CW_INST(3, 3, 2, 2, 2)
-    CW_INST(5, 5, 2, 4, 4)
-    CW_INST(4, 4, 1, 3, 3)
-    CW_INST(2, 2, 1, 1, 1)
-#undef CW_INST
+#define CW_NL(a, b, c, d, e, n)                                                 \
+    if (nl_sym == n) {                                                          \
+        *out = make_inst<a, b, c, d, e, n>();                                   \
+        return true;                                                            \
+    }
+    CW_GEO(4, 4, 2, 3, 3, 0)
+    CW_GEO(3, 3, 2, 2, 2, 0)
+    CW_GEO(5, 5, 2, 4, 4, 0)
+    CW_GEO(4, 4, 1, 3, 3, 0)
+#undef CW_NL
+#undef CW_GEO
     return false;
 }
 
@@ -86,7 +98,7 @@ struct cw_handle {
     float *d_state = nullptr, *d_that = nullptr, *d_coef = nullptr, *d_frames = nullptr;
     float *d_res = nullptr, *d_pred = nullptr, *d_dbg = nullptr;
     uint8_t *d_vidx = nullptr;
-    size_t state_floats = 0, that_floats = 0;
+    size_t state_floats = 0, that_floats = 0;  // floats (pairs x 2)
     long long frames_seen = 0;
     bool have_that = false;
     bool debug = false;
@@ -271,7 +283,10 @@ static int build_coef(cw_handle *h, const float *bank, const int64_t *retained, 
     auto flat = [&](int kz, int ky, int kx) { return ((kz + KZ) * My + (ky + KY)) * Mx + (kx + KX); };
     // the kernel holds z+ = Mz xhat+ (unnormalised DFT), S = norm * z+
     const double cS = 1.0 / std::sqrt((double)Mx * My * Mz);
-    const int NRET = Mz * WX * (2 * BY + 1);
+    // float2 pairs per velocity, in the kernel's retained z+ order:
+    // row 0: DC (kz = 0 real + zero pad, kz = 1..KZ), kx = 1..BX (all kz);
+    // rows ky = 1..BY: kx = -BX..BX (all kz)
+    const int NRET = 2 * ((KZ + 1) + BX * Mz + BY * WX * Mz);
     out->assign((size_t)h->nlx * h->nly * NRET, 0.f);
     for (int v = 0; v < h->nlx * h->nly; v++) {
         const float *bk = bank + (size_t)v * nret * 2;
@@ -298,6 +313,7 @@ static int build_coef(cw_handle *h, const float *bank, const int64_t *retained, 
         if (!coef(0, 0, 0, &cr, &ci))
             return CW_ERR_VALUE;
         o[w++] = (float)(cS * cr);
+        o[w++] = 0.f;  // pad: the DC kz = 0 state is real
         for (int kz = 1; kz <= KZ; kz++)
             if (!pair(kz, 0, 0))
                 return CW_ERR_VALUE;
@@ -333,8 +349,20 @@ int cw_create(const cw_params *p, int32_t width, int32_t height, int32_t device,
     int rc = check_params(p, width, height, &msg);
     if (rc != CW_OK)
         return fail(nullptr, rc, msg);
+    // symmetric odd grids with an exact 0 get the unrolled +-lag kernels
+    auto sym = [](const double *g, int n) {
+        if (n % 2 == 0 || g[n / 2] != 0.0)
+            return false;
+        for (int i = 0; i < n / 2; i++)
+            if (g[i] != -g[n - 1 - i])
+                return false;
+        return true;
+    };
+    const int nl_sym = (p->n_lag_x == p->n_lag_y && sym(p->lag_x, p->n_lag_x) && sym(p->lag_y, p->n_lag_y))
+                           ? p->n_lag_x
+                           : 0;
     LaunchFn fn;
-    if (!find_inst(p->kx, p->ky, p->kz, p->bx, p->by, &fn)) {
+    if (!find_inst(p->kx, p->ky, p->kz, p->bx, p->by, nl_sym, &fn)) {
         char buf[200];
         snprintf(buf, sizeof buf, "no compiled kernel for (kx,ky,kz,bx,by)=(%d,%d,%d,%d,%d)", p->kx, p->ky, p->kz,
                  p->bx, p->by);
@@ -398,8 +426,8 @@ int cw_create(const cw_params *p, int32_t width, int32_t height, int32_t device,
     h->grid = (int)std::min<long long>((long long)occ * sms, std::max<long long>(1, units / 2));
 
     const size_t pix_packets = (size_t)height * h->NXB;
-    h->state_floats = pix_packets * fn.ns * 32;
-    h->that_floats = pix_packets * fn.nt * 32;
+    h->state_floats = pix_packets * fn.nsp * 32 * 2;
+    h->that_floats = pix_packets * fn.ntp * 32 * 2;
     const size_t HW = (size_t)width * height;
     if (cudaMalloc(&h->d_state, h->state_floats * 4) != cudaSuccess ||
         cudaMalloc(&h->d_that, h->that_floats * 4) != cudaSuccess ||
@@ -495,13 +523,13 @@ static int run_frame(cw_handle *h, cudaStream_t s, int32_t *ready, int64_t *fram
     FrameArgs a;
     a.frame = h->d_frames + (size_t)(n % (h->mhz + 1)) * HW;
     a.delayed = rd ? h->d_frames + (size_t)(((n - h->mhz) % (h->mhz + 1))) * HW : nullptr;
-    a.state = h->d_state;
-    a.that = h->d_that;
-    a.coefP = h->d_coef;
+    a.state = reinterpret_cast<float2 *>(h->d_state);
+    a.that = reinterpret_cast<float2 *>(h->d_that);
+    a.coefP = reinterpret_cast<const float2 *>(h->d_coef);
     a.res = h->d_res;
     a.pred = h->d_pred;
     a.vidx = h->d_vidx;
-    a.dbgS = h->debug ? h->d_dbg : nullptr;
+    a.dbgS = h->debug ? reinterpret_cast<float2 *>(h->d_dbg) : nullptr;
     a.W = h->W;
     a.H = h->H;
     a.NXB = h->NXB;
@@ -665,6 +693,12 @@ int cw_read_view(cw_handle *h, int32_t what, void *dst, size_t bytes)
         CW_CUDA(h, cudaMemcpy(dst, h->d_state, bytes, cudaMemcpyDeviceToHost));
         return CW_OK;
     }
+    // pair j of pixel (y, x) in a packet buffer of `np` pairs per pixel
+    auto pairs_of = [&](const std::vector<float> &pk, int np, int y, int x, int j, double *re, double *im) {
+        const float *f = pk.data() + ((((size_t)y * NXB + x / 32) * np + j) * 32 + (x % 32)) * 2;
+        *re = f[0];
+        *im = f[1];
+    };
     if (what == 0) {
         const size_t nb = (size_t)Mx * My * Mz;
         if (bytes != (size_t)H * W * nb * 16)
@@ -674,33 +708,34 @@ int cw_read_view(cw_handle *h, int32_t what, void *dst, size_t bytes)
         std::vector<float> pk(h->state_floats);
         CW_CUDA(h, cudaMemcpy(pk.data(), h->d_dbg, h->state_floats * 4, cudaMemcpyDeviceToHost));
         double *o = static_cast<double *>(dst);
-        const int NS = h->fn.ns;
-        auto put = [&](size_t pixbase, int kz, int ky, int kx, double re, double im) {
-            size_t i = pixbase + (((size_t)(kz + KZ) * My + (ky + KY)) * Mx + (kx + KX));
-            o[2 * i] = re;
-            o[2 * i + 1] = im;
-            size_t j = pixbase + (((size_t)(-kz + KZ) * My + (-ky + KY)) * Mx + (-kx + KX));
-            o[2 * j] = re;
-            o[2 * j + 1] = -im;
-        };
+        const int NSP = h->fn.nsp;
+        const int row0 = (KZ + 1) + KX * Mz, rown = Mx * Mz;
         for (int y = 0; y < H; y++)
             for (int x = 0; x < W; x++) {
-                const float *f = pk.data() + ((size_t)y * NXB + x / 32) * NS * 32 + (x % 32);
-                auto F = [&](int j) { return (double)f[(size_t)j * 32]; };
                 const size_t pb = ((size_t)y * W + x) * nb;
-                put(pb, 0, 0, 0, F(0), 0.0);
-                for (int kz = 1; kz <= KZ; kz++)
-                    put(pb, kz, 0, 0, F(1 + 2 * (kz - 1)), F(2 + 2 * (kz - 1)));
+                auto put = [&](int kz, int ky, int kx, double re, double im) {
+                    size_t i = pb + (((size_t)(kz + KZ) * My + (ky + KY)) * Mx + (kx + KX));
+                    o[2 * i] = re;
+                    o[2 * i + 1] = im;
+                    size_t k = pb + (((size_t)(-kz + KZ) * My + (-ky + KY)) * Mx + (-kx + KX));
+                    o[2 * k] = re;
+                    o[2 * k + 1] = -im;
+                };
+                double re, im;
+                for (int kz = 0; kz <= KZ; kz++) {
+                    pairs_of(pk, NSP, y, x, kz, &re, &im);
+                    put(kz, 0, 0, re, kz == 0 ? 0.0 : im);
+                }
                 for (int kx = 1; kx <= KX; kx++)
                     for (int kz = -KZ; kz <= KZ; kz++) {
-                        const int j = Mz + (kx - 1) * 2 * Mz + 2 * (kz + KZ);
-                        put(pb, kz, 0, kx, F(j), F(j + 1));
+                        pairs_of(pk, NSP, y, x, KZ + 1 + (kx - 1) * Mz + (kz + KZ), &re, &im);
+                        put(kz, 0, kx, re, im);
                     }
                 for (int ky = 1; ky <= KY; ky++)
                     for (int kx = -KX; kx <= KX; kx++)
                         for (int kz = -KZ; kz <= KZ; kz++) {
-                            const int j = Mz * Mx + (ky - 1) * 2 * Mx * Mz + ((kx + KX) * Mz + (kz + KZ)) * 2;
-                            put(pb, kz, ky, kx, F(j), F(j + 1));
+                            pairs_of(pk, NSP, y, x, row0 + (ky - 1) * rown + (kx + KX) * Mz + (kz + KZ), &re, &im);
+                            put(kz, ky, kx, re, im);
                         }
             }
         return CW_OK;
@@ -712,27 +747,29 @@ int cw_read_view(cw_handle *h, int32_t what, void *dst, size_t bytes)
         std::vector<float> pk(h->that_floats);
         CW_CUDA(h, cudaMemcpy(pk.data(), h->d_that, h->that_floats * 4, cudaMemcpyDeviceToHost));
         double *o = static_cast<double *>(dst);
-        const int NT = h->fn.nt;
-        auto put = [&](size_t pb, int ky, int kx, double re, double im) {
-            size_t i = pb + (size_t)(ky + KY) * Mx + (kx + KX);
-            o[2 * i] = re;
-            o[2 * i + 1] = im;
-            size_t j = pb + (size_t)(-ky + KY) * Mx + (-kx + KX);
-            o[2 * j] = re;
-            o[2 * j + 1] = -im;
-        };
+        const int NTP = h->fn.ntp;
         for (int y = 0; y < H; y++)
             for (int x = 0; x < W; x++) {
-                const float *f = pk.data() + ((size_t)y * NXB + x / 32) * NT * 32 + (x % 32);
-                auto F = [&](int j) { return (double)f[(size_t)j * 32]; };
                 const size_t pb = ((size_t)y * W + x) * nt;
-                put(pb, 0, 0, F(0), 0.0);
-                for (int kx = 1; kx <= KX; kx++)
-                    put(pb, 0, kx, F(2 * kx - 1), F(2 * kx));
+                auto put = [&](int ky, int kx, double re, double im) {
+                    size_t i = pb + (size_t)(ky + KY) * Mx + (kx + KX);
+                    o[2 * i] = re;
+                    o[2 * i + 1] = im;
+                    size_t k = pb + (size_t)(-ky + KY) * Mx + (-kx + KX);
+                    o[2 * k] = re;
+                    o[2 * k + 1] = -im;
+                };
+                double re, im;
+                pairs_of(pk, NTP, y, x, 0, &re, &im);
+                put(0, 0, re, 0.0);
+                for (int kx = 1; kx <= KX; kx++) {
+                    pairs_of(pk, NTP, y, x, kx, &re, &im);
+                    put(0, kx, re, im);
+                }
                 for (int ky = 1; ky <= KY; ky++)
                     for (int kx = -KX; kx <= KX; kx++) {
-                        const int j = Mx + (ky - 1) * 2 * Mx + 2 * (kx + KX);
-                        put(pb, ky, kx, F(j), F(j + 1));
+                        pairs_of(pk, NTP, y, x, (KX + 1) + (ky - 1) * Mx + (kx + KX), &re, &im);
+                        put(ky, kx, re, im);
                     }
             }
         return CW_OK;

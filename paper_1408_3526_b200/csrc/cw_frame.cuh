@@ -4,7 +4,7 @@
 // Pipeline.process_frame (/root/reference/pkg/src/clutterwhiten/
 // pipeline.py:201-294):
 //
-//   spatial SDFT (x: 9-tap window sums, y: comb + resonator recursion,
+//   spatial SDFT (x: Mx-tap window sums, y: comb + resonator recursion,
 //                 _kernels.py:31-68)
 //   temporal deadbeat observer (replaces the ring DFT, _kernels.py:71-90)
 //   DC suppression + 3-D Hann + power (_kernels.py:156-227)
@@ -18,9 +18,15 @@
 // column) and one warp per spatial-frequency row ky = 0..KY (real input =>
 // conjugate symmetry, only the half space is kept).  It walks a contiguous
 // run of the linearised (column-block, row) space, carrying the y-SDFT
-// resonator state in registers from row to row.  Per-pixel state lives in
-// HBM in "packet" layout [row*NXB + xb][float j][lane]: every warp access
-// is one full 128-byte line.
+// resonator state in registers from row to row.
+//
+// Per-pixel state lives in HBM as "packets": for a (row, 32-column block),
+// the observer state is float2 P[pair][lane] (re/im pairs, lane-minor), so
+// one (row, block) is a single contiguous 52 KB span.  Each row's packet is
+// brought into shared memory by TMA bulk copies (cp.async.bulk + mbarrier)
+// issued a phase ahead; the observer writes the updated state straight back
+// to HBM with 256-byte coalesced stores and overwrites the staged copy in
+// place with the Hann-conditioned spectrum that the neighbouring rows need.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -30,10 +36,7 @@ namespace cwb {
 constexpr int MAXK = 5;    // largest half window supported by the tables
 constexpr int MAXM = 2 * MAXK + 1;
 constexpr int MAXL = 33;   // largest lag grid per axis
-constexpr int RESTART = 32;
-#ifndef CW_MINB
-#define CW_MINB 2  // resident CTAs per SM the register budget is sized for
-#endif  // rows between direct y-SDFT restarts (bounds f32 drift)
+constexpr int RESTART = 32;  // rows between direct y-SDFT restarts (bounds f32 drift)
 
 struct Tables {
     // x stage: cos/sin(2 pi kx m / Mx), kx = 0..KX, m = 0..Mx-1
@@ -64,13 +67,13 @@ struct Tables {
 struct FrameArgs {
     const float *frame;    // (H, W) current frame (local strip)
     const float *delayed;  // (H, W) frame n - mhat_z (nullptr until ready)
-    float *state;          // observer state, packets [H*NXB][NS][32]
-    float *that;           // smoothing state T^, packets [H*NXB][NT][32]
-    const float *coefP;    // PEF coefficients [Ly*Lx][NRET]
+    float2 *state;         // observer state packets [H*NXB][NSP][32]
+    float2 *that;          // smoothing state T^ packets [H*NXB][NTP][32]
+    const float2 *coefP;   // PEF coefficients [Ly*Lx][RETP]
     float *res;            // (H, W) residual out
     float *pred;           // (H, W) prediction out (nullable)
     uint8_t *vidx;         // (H, W, 2) velocity index out
-    float *dbgS;           // spectrum dump, packets [H*NXB][NS][32] (nullable)
+    float2 *dbgS;          // spectrum dump, state-packet layout (nullable)
     int W, H, NXB;
     int y_begin;           // first local anchor row (strip halo)
     int y_off;             // global row of local row 0
@@ -86,35 +89,42 @@ struct Geo {
     static constexpr int WX = 2 * BX + 1, WY = 2 * BY + 1;
     static constexpr int NR = KY + 1;            // warps = spatial-frequency rows
     static constexpr int NTHREADS = 32 * NR;
-    static constexpr int NS = MX * MY * MZ;       // observer floats per pixel
-    static constexpr int ROW0 = MZ * MX;          // ... in row ky = 0
-    static constexpr int ROWN = 2 * MX * MZ;      // ... in rows ky >= 1
-    static constexpr int NT = MX * MY;            // T^ floats per pixel
-    static constexpr int TROW0 = MX, TROWN = 2 * MX;
-    static constexpr int NRET = MZ * WX * WY;     // retained floats (== coefficient count)
-    static constexpr int PROW0 = MZ * WX, PROWN = 2 * MZ * WX;
+    // observer state pairs per pixel: row 0 = DC bin (kz = 0 real + pad,
+    // kz = 1..KZ) + kx = 1..KX (all kz); rows >= 1 = MX * MZ
+    static constexpr int ROW0P = (KZ + 1) + KX * MZ;
+    static constexpr int ROWNP = MX * MZ;
+    static constexpr int NSP = ROW0P + KY * ROWNP;
+    // T^ pairs: row 0 = T(0,0) real + pad, kx = 1..KX; rows >= 1 = MX
+    static constexpr int TROW0P = KX + 1, TROWNP = MX;
+    static constexpr int NTP = TROW0P + KY * TROWNP;
+    // retained z+ pairs (== PEF coefficient pairs)
+    static constexpr int PROW0P = (KZ + 1) + BX * MZ, PROWNP = WX * MZ;
+    static constexpr int RETP = PROW0P + BY * PROWNP;
     static constexpr int RING = MY + 2;           // x-stage ring rows
     static constexpr int XF = MX;                 // x-stage floats per (row, col)
-    __host__ __device__ static constexpr int srow(int r) { return r == 0 ? 0 : ROW0 + (r - 1) * ROWN; }
-    __host__ __device__ static constexpr int trow(int r) { return r == 0 ? 0 : TROW0 + (r - 1) * TROWN; }
-    __host__ __device__ static constexpr int prow(int r) { return r == 0 ? 0 : PROW0 + (r - 1) * PROWN; }
-    // shared memory plan (floats)
-    static constexpr int SM_XF = RING * XF * 32;
-    static constexpr int SM_CX = NR * MZ * MX * 2 * 32;
-    static constexpr int SM_BB = NR * MAXL * 2 * 32;
-    static constexpr int SM_CXBB = SM_CX > SM_BB ? SM_CX : SM_BB;
-    static constexpr int SM_RET = NRET * 32;
-    static constexpr int SM_BEST = NR * 32 * 2;
-    static constexpr int SM_PEF = (BY + 1) * 32;
-    static constexpr int SM_RANK = (MAXL * MAXL + 1) / 2;  // uint16 rank table
-    static constexpr int SMEM_FLOATS = SM_XF + SM_CXBB + SM_RET + SM_BEST + SM_PEF + SM_RANK;
-    static constexpr size_t SMEM_BYTES = sizeof(float) * SMEM_FLOATS;
+    __host__ __device__ static constexpr int spair(int r) { return r == 0 ? 0 : ROW0P + (r - 1) * ROWNP; }
+    __host__ __device__ static constexpr int tpair(int r) { return r == 0 ? 0 : TROW0P + (r - 1) * TROWNP; }
+    __host__ __device__ static constexpr int ppair(int r) { return r == 0 ? 0 : PROW0P + (r - 1) * PROWNP; }
+    // shared memory plan (bytes); the stage also holds B(ky, lx) = NR x MAXL pairs
+    static constexpr int STAGEP = NSP > NR * MAXL ? NSP : NR * MAXL;
+    static constexpr int SM_STAGE = STAGEP * 32 * 8;  // state packet -> Cx in place -> B(ky,lx)
+    static constexpr int SM_TSTAGE = NTP * 32 * 8;    // T^ packet
+    static constexpr int SM_RET = RETP * 32 * 8;      // retained z+
+    static constexpr int SM_XF = RING * XF * 32 * 4;  // x-stage ring
+    static constexpr int SM_BEST = NR * 32 * 8;       // partial argmax (score, rank)
+    static constexpr int SM_PEF = (BY + 1) * 32 * 4;
+    static constexpr int SM_RANK = ((MAXL * MAXL * 2) + 15) / 16 * 16;
+    static constexpr int SM_BAR = 16;
+    static constexpr size_t SMEM_BYTES =
+        SM_STAGE + SM_TSTAGE + SM_RET + SM_XF + SM_BEST + SM_PEF + SM_RANK + SM_BAR;
 };
 
 struct cf {
     float r, i;
 };
 __device__ __forceinline__ cf cmk(float r, float i) { return cf{r, i}; }
+__device__ __forceinline__ cf c2(float2 v) { return cf{v.x, v.y}; }
+__device__ __forceinline__ float2 f2(cf v) { return make_float2(v.r, v.i); }
 __device__ __forceinline__ cf cadd(cf a, cf b) { return cf{a.r + b.r, a.i + b.i}; }
 __device__ __forceinline__ cf csub(cf a, cf b) { return cf{a.r - b.r, a.i - b.i}; }
 __device__ __forceinline__ cf cmul(cf a, cf b) { return cf{a.r * b.r - a.i * b.i, a.r * b.i + a.i * b.r}; }
@@ -133,38 +143,93 @@ __device__ __forceinline__ bool better(float v, int rk, float best, int brk)
     return v > best || (v == best && rk < brk);
 }
 
-template <class G>
-__global__ void __launch_bounds__(G::NTHREADS, CW_MINB)
+// ---- TMA bulk copy + mbarrier (PTX) ----------------------------------------
+__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase)
+{
+    uint32_t ok = 0;
+    do {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(ok)
+            : "r"(smem_addr(bar)), "r"(phase)
+            : "memory");
+    } while (!ok);
+}
+
+template <class G, int NL>
+__global__ void __launch_bounds__(G::NTHREADS, 2)
 cw_frame_kernel(const FrameArgs a, const Tables t)
 {
     constexpr int KX = G::KX, KY = G::KY, KZ = G::KZ, BX = G::BX, BY = G::BY;
     constexpr int MX = G::MX, MY = G::MY, MZ = G::MZ;
     constexpr int NR = G::NR, RING = G::RING;
 
-    extern __shared__ float smem[];
-    float *xfr = smem;                      // [RING][XF][32]       x-stage ring
-    float *cxb = xfr + G::SM_XF;            // [NR][MZ][MX][2][32]  Hy exchange
-    float *bb = cxb;                        // [NR][MAXL][2][32]    stage-1 exchange (aliased)
-    float *sret = cxb + G::SM_CXBB;         // [NRET][32]           retained z+
-    float *pbest = sret + G::SM_RET;        // [NR][32] score
-    int *prank = reinterpret_cast<int *>(pbest + NR * 32);  // [NR][32]
-    float *ppef = pbest + G::SM_BEST;       // [BY+1][32]
-    uint16_t *srank = reinterpret_cast<uint16_t *>(ppef + G::SM_PEF);  // [nly][nlx]
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    float2 *stage = reinterpret_cast<float2 *>(smem_raw);                       // [NSP][32]
+    float2 *tstage = reinterpret_cast<float2 *>(smem_raw + G::SM_STAGE);        // [NTP][32]
+    float2 *sret = reinterpret_cast<float2 *>(smem_raw + G::SM_STAGE + G::SM_TSTAGE);  // [RETP][32]
+    float *xfr = reinterpret_cast<float *>(smem_raw + G::SM_STAGE + G::SM_TSTAGE + G::SM_RET);
+    float2 *pbest = reinterpret_cast<float2 *>(smem_raw + G::SM_STAGE + G::SM_TSTAGE + G::SM_RET + G::SM_XF);
+    float *ppef = reinterpret_cast<float *>(reinterpret_cast<unsigned char *>(pbest) + G::SM_BEST);
+    uint16_t *srank = reinterpret_cast<uint16_t *>(reinterpret_cast<unsigned char *>(ppef) + G::SM_PEF);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(reinterpret_cast<unsigned char *>(srank) + G::SM_RANK);
+    float2 *bb = stage;  // B(ky, lx) after the Hy reads: [NR][MAXL][32]
 
     const int lane = threadIdx.x & 31;
     const int r = threadIdx.x >> 5;  // spatial-frequency row ky of this warp
     const int W = a.W, H = a.H, NXB = a.NXB;
-    const int nlx = t.nlx, nly = t.nly;
+    const int nlx = NL ? NL : t.nlx, nly = NL ? NL : t.nly;
     const int rows = H - a.y_begin;
     const long long units = (long long)NXB * rows;
     const long long u0 = units * blockIdx.x / gridDim.x;
     const long long u1 = units * (blockIdx.x + 1) / gridDim.x;
+    const bool use_that = a.ready && !a.first;
 
     for (int i = threadIdx.x; i < nlx * nly; i += G::NTHREADS) srank[i] = t.rank[i];
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    uint32_t phase = 0;
+
+    // one elected thread stages the (row, block) packets of the next row
+    auto issue = [&](int yy, int xb) {
+        if (threadIdx.x == 0) {
+            const size_t pix = (size_t)yy * NXB + xb;
+            fence_proxy_async();  // prior generic smem accesses before the async-proxy writes
+            const uint32_t bs = G::NSP * 32 * 8, bt = use_that ? G::SM_TSTAGE : 0;
+            mbar_expect_tx(bar, bs + bt);
+            const unsigned char *src = reinterpret_cast<const unsigned char *>(a.state + pix * G::NSP * 32);
+            constexpr uint32_t CH = (G::NSP * 32 * 8 / 4 + 15) / 16 * 16;
+            for (uint32_t off = 0; off < bs; off += CH)
+                tma_load(reinterpret_cast<unsigned char *>(stage) + off, src + off, (bs - off) < CH ? (bs - off) : CH,
+                         bar);
+            if (bt) tma_load(tstage, a.that + pix * G::NTP * 32, bt, bar);
+        }
+    };
 
 #define XFR(slot, f) xfr[((slot) * G::XF + (f)) * 32 + lane]
-#define CXB(rr, kzi, kxi, c) cxb[((((rr) * MZ + (kzi)) * MX + (kxi)) * 2 + (c)) * 32 + lane]
-#define BB(rr, lx, c) bb[(((rr) * MAXL + (lx)) * 2 + (c)) * 32 + lane]
 
     // x stage for local row yy at column x: Mx-tap window sums (the row
     // sweep, _kernels.py:31-45), zero outside the frame; kx = 0 real.
@@ -195,23 +260,17 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
         if (kx > 0) return cmk(XFR(slot, 2 * kx - 1), XFR(slot, 2 * kx));
         return cmk(XFR(slot, -2 * kx - 1), -XFR(slot, -2 * kx));
     };
-    // this warp's observer floats and T^ floats of pixel row yy (registers)
-    const int nst = (r == 0) ? G::ROW0 : G::ROWN;
-    const int nth = (r == 0) ? G::TROW0 : G::TROWN;
-    float st[G::ROWN];
-    float thv[G::TROWN];
-    auto load_rows = [&](int yy, int xb, bool with_that) {
-        const size_t pix = (size_t)yy * NXB + xb;
-        const float *sp_ = a.state + (pix * G::NS + G::srow(r)) * 32 + lane;
-#pragma unroll
-        for (int j = 0; j < G::ROWN; j++)
-            if (j < nst) st[j] = sp_[j * 32];
-        if (with_that) {
-            const float *tp = a.that + (pix * G::NT + G::trow(r)) * 32 + lane;
-#pragma unroll
-            for (int j = 0; j < G::TROWN; j++)
-                if (j < nth) thv[j] = tp[j * 32];
+    // Cx of row rr at (kz, kx), any kx: row 0 is stored compact (kx >= 0)
+    auto cx_at = [&](int rr, int kz, int kx) -> cf {
+        if (rr == 0) {
+            if (kx == 0) {
+                const cf v = c2(stage[(kz >= 0 ? kz : -kz) * 32 + lane]);
+                return kz >= 0 ? v : cconj(v);
+            }
+            if (kx > 0) return c2(stage[(KZ + 1 + (kx - 1) * MZ + (kz + KZ)) * 32 + lane]);
+            return cconj(c2(stage[(KZ + 1 + (-kx - 1) * MZ + (-kz + KZ)) * 32 + lane]));
         }
+        return c2(stage[(G::spair(rr) + (kx + KX) * MZ + (kz + KZ)) * 32 + lane]);
     };
 
     long long u = u0;
@@ -223,12 +282,13 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
         const int x = xb * 32 + lane;
         const bool colv = x < W;
 
-        __syncthreads();  // ring reuse across chunks
+        fence_proxy_async();
+        __syncthreads();  // previous chunk done with the stage and the ring
+        issue(ys, xb);
         for (int k = r; k < MY; k += NR) {
             const int yy = ys - MY + 1 + k;
             xstage(yy, x, ring_slot(yy));
         }
-        load_rows(ys, xb, a.ready && !a.first);
         __syncthreads();
 
         cf sp[MX];  // y-SDFT resonators of row ky = r, kx = -KX..KX
@@ -257,8 +317,11 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
             }
             const bool anchor = colv && x >= MX - 1 && (yy + a.y_off) >= MY - 1;
             const size_t pix = (size_t)yy * NXB + xb;
-            float *stg = a.state + (pix * G::NS + G::srow(r)) * 32 + lane;
-            float *dbg = a.dbgS ? a.dbgS + (pix * G::NS + G::srow(r)) * 32 + lane : nullptr;
+            float2 *stg = a.state + (pix * G::NSP + G::spair(r)) * 32 + lane;
+            float2 *dbg = a.dbgS ? a.dbgS + (pix * G::NSP + G::spair(r)) * 32 + lane : nullptr;
+            float2 *sst = stage + G::spair(r) * 32 + lane;
+            mbar_wait(bar, phase);
+            phase ^= 1;
 
             // Deadbeat observer on z = Mz * xhat (state in HBM, in place):
             //   e = u - (1/Mz) sum_kz z ;  z+ = z + e ;  z <- w(kz) z+
@@ -268,26 +331,23 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
             if (r == 0) {
                 {   // DC spatial bin: real input; z(0) real, z(1..KZ) complex
                     const float uv = anchor ? sp[KX].r : 0.f;
-                    float sum = st[0];
+                    cf zd[KZ + 1];
 #pragma unroll
-                    for (int kz = 1; kz <= KZ; kz++) sum = fmaf(2.f, st[2 * kz - 1], sum);
+                    for (int kz = 0; kz <= KZ; kz++) zd[kz] = c2(sst[kz * 32]);
+                    float sum = zd[0].r;
+#pragma unroll
+                    for (int kz = 1; kz <= KZ; kz++) sum = fmaf(2.f, zd[kz].r, sum);
                     const float e = fmaf(-t.inv_mz, sum, uv);
-                    const float z0 = st[0] + e;
-                    stg[0] = z0;
-                    sret[lane] = z0;
-                    if (dbg) dbg[0] = t.norm * z0;
+                    const float z0 = zd[0].r + e;
+                    stg[0] = make_float2(z0, 0.f);
+                    sret[lane] = make_float2(z0, 0.f);
+                    if (dbg) dbg[0] = make_float2(t.norm * z0, 0.f);
 #pragma unroll
                     for (int kz = 1; kz <= KZ; kz++) {
-                        const cf zp = cmk(st[2 * kz - 1] + e, st[2 * kz]);
-                        const cf zn = cmul(cmk(t.wc[kz + KZ], t.ws[kz + KZ]), zp);
-                        stg[(2 * kz - 1) * 32] = zn.r;
-                        stg[(2 * kz) * 32] = zn.i;
-                        sret[(2 * kz - 1) * 32 + lane] = zp.r;
-                        sret[(2 * kz) * 32 + lane] = zp.i;
-                        if (dbg) {
-                            dbg[(2 * kz - 1) * 32] = t.norm * zp.r;
-                            dbg[(2 * kz) * 32] = t.norm * zp.i;
-                        }
+                        const cf zp = cmk(zd[kz].r + e, zd[kz].i);
+                        stg[kz * 32] = f2(cmul(cmk(t.wc[kz + KZ], t.ws[kz + KZ]), zp));
+                        sret[kz * 32 + lane] = f2(zp);
+                        if (dbg) dbg[kz * 32] = make_float2(t.norm * zp.r, t.norm * zp.i);
                     }
                 }
                 // DC suppression (_kernels.py:167-174): C(kz, 0, 0) = 0
@@ -295,27 +355,24 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                 for (int kzi = 0; kzi < MZ; kzi++) cz[KX][kzi] = cmk(0.f, 0.f);
 #pragma unroll
                 for (int kx = 1; kx <= KX; kx++) {
-                    const int base = MZ + (kx - 1) * 2 * MZ;
+                    const int base = KZ + 1 + (kx - 1) * MZ;
                     const cf uv = anchor ? sp[KX + kx] : cmk(0.f, 0.f);
+                    cf z[MZ];
                     cf sum = cmk(0.f, 0.f);
 #pragma unroll
-                    for (int kzi = 0; kzi < MZ; kzi++) sum = cadd(sum, cmk(st[base + 2 * kzi], st[base + 2 * kzi + 1]));
+                    for (int kzi = 0; kzi < MZ; kzi++) {
+                        z[kzi] = c2(sst[(base + kzi) * 32]);
+                        sum = cadd(sum, z[kzi]);
+                    }
                     const cf e = cmk(fmaf(-t.inv_mz, sum.r, uv.r), fmaf(-t.inv_mz, sum.i, uv.i));
                     cf zp[MZ];
 #pragma unroll
                     for (int kzi = 0; kzi < MZ; kzi++) {
-                        zp[kzi] = cmk(st[base + 2 * kzi] + e.r, st[base + 2 * kzi + 1] + e.i);
+                        zp[kzi] = cadd(z[kzi], e);
                         const cf zn = (kzi == KZ) ? zp[kzi] : cmul(cmk(t.wc[kzi], t.ws[kzi]), zp[kzi]);
-                        stg[(base + 2 * kzi) * 32] = zn.r;
-                        stg[(base + 2 * kzi + 1) * 32] = zn.i;
-                        if (kx <= BX) {
-                            sret[(base + 2 * kzi) * 32 + lane] = zp[kzi].r;
-                            sret[(base + 2 * kzi + 1) * 32 + lane] = zp[kzi].i;
-                        }
-                        if (dbg) {
-                            dbg[(base + 2 * kzi) * 32] = t.norm * zp[kzi].r;
-                            dbg[(base + 2 * kzi + 1) * 32] = t.norm * zp[kzi].i;
-                        }
+                        stg[(base + kzi) * 32] = f2(zn);
+                        if (kx <= BX) sret[(base + kzi) * 32 + lane] = f2(zp[kzi]);
+                        if (dbg) dbg[(base + kzi) * 32] = make_float2(t.norm * zp[kzi].r, t.norm * zp[kzi].i);
                     }
 #pragma unroll
                     for (int kzi = 0; kzi < MZ; kzi++)
@@ -326,128 +383,145 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                 for (int kx = 1; kx <= KX; kx++)
 #pragma unroll
                     for (int kzi = 0; kzi < MZ; kzi++) cz[KX - kx][kzi] = cconj(cz[KX + kx][MZ - 1 - kzi]);
+                if (a.ready) {
+                    // Hx, compact row 0 in place: kx = 0 (kz = 0..KZ), kx = 1..KX (all kz)
+#pragma unroll
+                    for (int kz = 0; kz <= KZ; kz++) {
+                        const cf h = hann4(cz[KX - 1][kz + KZ], cz[KX][kz + KZ], cz[KX + 1][kz + KZ]);
+                        sst[kz * 32] = kz == 0 ? make_float2(h.r, 0.f) : f2(h);
+                    }
+#pragma unroll
+                    for (int kx = 1; kx <= KX; kx++)
+#pragma unroll
+                        for (int kzi = 0; kzi < MZ; kzi++) {
+                            const int kxi = KX + kx;
+                            const cf h = hann4(cz[kxi - 1][kzi], cz[kxi][kzi], cz[(kxi + 1) % MX][kzi]);
+                            sst[(KZ + 1 + (kx - 1) * MZ + kzi) * 32] = f2(h);
+                        }
+                }
             } else {
-                float *rr = sret + G::prow(r <= BY ? r : 0) * 32 + lane;
+                float2 *rr = sret + G::ppair(r <= BY ? r : 0) * 32 + lane;
 #pragma unroll
                 for (int kxi = 0; kxi < MX; kxi++) {
-                    const int base = kxi * MZ * 2;
                     const cf uv = anchor ? sp[kxi] : cmk(0.f, 0.f);
+                    cf z[MZ];
                     cf sum = cmk(0.f, 0.f);
 #pragma unroll
-                    for (int kzi = 0; kzi < MZ; kzi++) sum = cadd(sum, cmk(st[base + 2 * kzi], st[base + 2 * kzi + 1]));
+                    for (int kzi = 0; kzi < MZ; kzi++) {
+                        z[kzi] = c2(sst[(kxi * MZ + kzi) * 32]);
+                        sum = cadd(sum, z[kzi]);
+                    }
                     const cf e = cmk(fmaf(-t.inv_mz, sum.r, uv.r), fmaf(-t.inv_mz, sum.i, uv.i));
                     cf zp[MZ];
                     const int kxb = kxi - KX + BX;  // retained-band column
 #pragma unroll
                     for (int kzi = 0; kzi < MZ; kzi++) {
-                        zp[kzi] = cmk(st[base + 2 * kzi] + e.r, st[base + 2 * kzi + 1] + e.i);
+                        zp[kzi] = cadd(z[kzi], e);
                         const cf zn = (kzi == KZ) ? zp[kzi] : cmul(cmk(t.wc[kzi], t.ws[kzi]), zp[kzi]);
-                        stg[(base + 2 * kzi) * 32] = zn.r;
-                        stg[(base + 2 * kzi + 1) * 32] = zn.i;
-                        if (r <= BY && kxb >= 0 && kxb < G::WX) {
-                            rr[((kxb * MZ + kzi) * 2) * 32] = zp[kzi].r;
-                            rr[((kxb * MZ + kzi) * 2 + 1) * 32] = zp[kzi].i;
-                        }
-                        if (dbg) {
-                            dbg[(base + 2 * kzi) * 32] = t.norm * zp[kzi].r;
-                            dbg[(base + 2 * kzi + 1) * 32] = t.norm * zp[kzi].i;
-                        }
+                        stg[(kxi * MZ + kzi) * 32] = f2(zn);
+                        if (r <= BY && kxb >= 0 && kxb < G::WX) rr[(kxb * MZ + kzi) * 32] = f2(zp[kzi]);
+                        if (dbg) dbg[(kxi * MZ + kzi) * 32] = make_float2(t.norm * zp[kzi].r, t.norm * zp[kzi].i);
                     }
 #pragma unroll
                     for (int kzi = 0; kzi < MZ; kzi++)
                         cz[kxi][kzi] = hann4(zp[(kzi + MZ - 1) % MZ], zp[kzi], zp[(kzi + 1) % MZ]);
                 }
-            }
-            if (a.ready) {
-                // Hx (circular along kx), full row to shared memory
+                if (a.ready) {
+                    // Hx (circular along kx), in place over this row's staged state
 #pragma unroll
-                for (int kzi = 0; kzi < MZ; kzi++)
+                    for (int kxi = 0; kxi < MX; kxi++)
 #pragma unroll
-                    for (int kxi = 0; kxi < MX; kxi++) {
-                        const cf h = hann4(cz[(kxi + MX - 1) % MX][kzi], cz[kxi][kzi], cz[(kxi + 1) % MX][kzi]);
-                        CXB(r, kzi, kxi, 0) = h.r;
-                        CXB(r, kzi, kxi, 1) = h.i;
-                    }
+                        for (int kzi = 0; kzi < MZ; kzi++) {
+                            const cf h = hann4(cz[(kxi + MX - 1) % MX][kzi], cz[kxi][kzi], cz[(kxi + 1) % MX][kzi]);
+                            sst[(kxi * MZ + kzi) * 32] = f2(h);
+                        }
+                }
             }
+            if (!a.ready) fence_proxy_async();  // stage reads before the next TMA write
             __syncthreads();  // (1) Cx rows visible; x stage of yy+1 done
+            if (!a.ready) {
+                if (yy + 1 < ye) issue(yy + 1, xb);  // stage free: next row's state
+                continue;
+            }
 
             // ---------------- phase C1: Hy, power, kz collapse, smoothing ----------------
             cf T[MX];
-            if (a.ready) {
-                const int klo = (r == 0) ? KX : 0;  // row 0: kx >= 0 only
-#pragma unroll
-                for (int kxi = 0; kxi < MX; kxi++) {
-                    T[kxi] = cmk(0.f, 0.f);
-                    if (kxi < klo) continue;
-#pragma unroll
-                    for (int kzi = 0; kzi < MZ; kzi++) {
-                        const cf own = cmk(CXB(r, kzi, kxi, 0), CXB(r, kzi, kxi, 1));
-                        cf up, dn;
-                        if (r == 0) {  // row -1 = conj-flip of row 1
-                            up = cmk(CXB(1, MZ - 1 - kzi, MX - 1 - kxi, 0), -CXB(1, MZ - 1 - kzi, MX - 1 - kxi, 1));
-                            dn = cmk(CXB(1, kzi, kxi, 0), CXB(1, kzi, kxi, 1));
-                        } else {
-                            up = cmk(CXB(r - 1, kzi, kxi, 0), CXB(r - 1, kzi, kxi, 1));
-                            if (r < KY)
-                                dn = cmk(CXB(r + 1, kzi, kxi, 0), CXB(r + 1, kzi, kxi, 1));
-                            else  // row KY+1 == -KY = conj-flip of row KY
-                                dn = cmk(CXB(KY, MZ - 1 - kzi, MX - 1 - kxi, 0), -CXB(KY, MZ - 1 - kzi, MX - 1 - kxi, 1));
-                        }
-                        const cf c = hann4(up, own, dn);
-                        const float p = fmaf(c.r, c.r, c.i * c.i);
-                        T[kxi].r = fmaf(t.azc[kzi], p, T[kxi].r);
-                        T[kxi].i = fmaf(t.azs[kzi], p, T[kxi].i);
-                    }
-                }
-                // smoothing of T^ (_kernels.py:261-271; first ready frame copies)
-                float *th = a.that + (pix * G::NT + G::trow(r)) * 32 + lane;
+            {
+                float2 *thg = a.that + (pix * G::NTP + G::tpair(r)) * 32 + lane;
+                const float2 *tho = tstage + G::tpair(r) * 32 + lane;
                 if (r == 0) {
+#pragma unroll
+                    for (int kx = 0; kx <= KX; kx++) {
+                        cf acc = cmk(0.f, 0.f);
+#pragma unroll
+                        for (int kz = -KZ; kz <= KZ; kz++) {
+                            // row -1 = conj-flip of row 1
+                            const cf up = cconj(cx_at(1, -kz, -kx));
+                            const cf c = hann4(up, cx_at(0, kz, kx), cx_at(1, kz, kx));
+                            const float p = fmaf(c.r, c.r, c.i * c.i);
+                            acc.r = fmaf(t.azc[kz + KZ], p, acc.r);
+                            acc.i = fmaf(t.azs[kz + KZ], p, acc.i);
+                        }
+                        T[KX + kx] = acc;
+                    }
+                    // smoothing of T^ (_kernels.py:261-271; first ready frame copies)
                     float v = T[KX].r;
-                    if (!a.first) v = fmaf(t.beta, v, t.alpha * thv[0]);
-                    th[0] = v;
+                    if (!a.first) v = fmaf(t.beta, v, t.alpha * tho[0].x);
+                    thg[0] = make_float2(v, 0.f);
                     T[KX] = cmk(v, 0.f);
 #pragma unroll
                     for (int kx = 1; kx <= KX; kx++) {
                         cf v2 = T[KX + kx];
-                        if (!a.first)
-                            v2 = cmk(fmaf(t.beta, v2.r, t.alpha * thv[2 * kx - 1]), fmaf(t.beta, v2.i, t.alpha * thv[2 * kx]));
-                        th[(2 * kx - 1) * 32] = v2.r;
-                        th[(2 * kx) * 32] = v2.i;
+                        if (!a.first) {
+                            const float2 o = tho[kx * 32];
+                            v2 = cmk(fmaf(t.beta, v2.r, t.alpha * o.x), fmaf(t.beta, v2.i, t.alpha * o.y));
+                        }
+                        thg[kx * 32] = f2(v2);
                         T[KX + kx] = v2;
                     }
                 } else {
 #pragma unroll
                     for (int kxi = 0; kxi < MX; kxi++) {
-                        cf v2 = T[kxi];
-                        if (!a.first)
-                            v2 = cmk(fmaf(t.beta, v2.r, t.alpha * thv[2 * kxi]), fmaf(t.beta, v2.i, t.alpha * thv[2 * kxi + 1]));
-                        th[(2 * kxi) * 32] = v2.r;
-                        th[(2 * kxi + 1) * 32] = v2.i;
+                        cf acc = cmk(0.f, 0.f);
+#pragma unroll
+                        for (int kzi = 0; kzi < MZ; kzi++) {
+                            const int kz = kzi - KZ, kx = kxi - KX;
+                            const cf up = cx_at(r - 1, kz, kx);
+                            // row KY+1 == -KY = conj-flip of row KY
+                            const cf dn = (r < KY) ? cx_at(r + 1, kz, kx) : cconj(cx_at(KY, -kz, -kx));
+                            const cf c = hann4(up, cx_at(r, kz, kx), dn);
+                            const float p = fmaf(c.r, c.r, c.i * c.i);
+                            acc.r = fmaf(t.azc[kzi], p, acc.r);
+                            acc.i = fmaf(t.azs[kzi], p, acc.i);
+                        }
+                        cf v2 = acc;
+                        if (!a.first) {
+                            const float2 o = tho[kxi * 32];
+                            v2 = cmk(fmaf(t.beta, v2.r, t.alpha * o.x), fmaf(t.beta, v2.i, t.alpha * o.y));
+                        }
+                        thg[kxi * 32] = f2(v2);
                         T[kxi] = v2;
                     }
                 }
             }
-            // prefetch the next row's observer and T^ rows (consumed after the
-            // remaining phases: hides the HBM latency behind them)
-            if (yy + 1 < ye) load_rows(yy + 1, xb, a.ready && !a.first);
-            if (!a.ready) continue;
-            __syncthreads();  // (2) Hy reads of cxb done before bb overwrites it
+            __syncthreads();  // (2) Hy reads of the stage done: it now holds B(ky, lx)
 
             // ---------------- phase C2: stage-1 lag contraction along kx ----------------
             // B(ky, lx) = gx(lx) sum_kx e^{-j 2 pi kx lx / Mx} T^(ky, kx)
-            if (t.sym_x) {
-                const int c0 = nlx >> 1;  // lag 0; lags +-p at c0 +- p
+#define BB(rr, lx) bb[((rr) * MAXL + (lx)) * 32 + lane]
+            if (NL && t.sym_x) {
+                constexpr int C0 = NL / 2;  // lag 0; lags +-q at C0 +- q
                 if (r == 0) {
-                    for (int q = 0; q <= c0; q++) {
-                        const int lx = c0 + q;
-                        float cp = t.s1g[lx] * T[KX].r, sp2 = 0.f;
+#pragma unroll
+                    for (int q = 0; q <= C0; q++) {
+                        float cp = t.s1g[C0 + q] * T[KX].r, sp2 = 0.f;
 #pragma unroll
                         for (int kx = 1; kx <= KX; kx++) {
-                            cp = fmaf(2.f * t.s1c[lx][kx - 1], T[KX + kx].r, cp);
-                            sp2 = fmaf(2.f * t.s1s[lx][kx - 1], T[KX + kx].i, sp2);
+                            cp = fmaf(2.f * t.s1c[C0 + q][kx - 1], T[KX + kx].r, cp);
+                            sp2 = fmaf(2.f * t.s1s[C0 + q][kx - 1], T[KX + kx].i, sp2);
                         }
-                        BB(0, c0 + q, 0) = cp + sp2;
-                        BB(0, c0 - q, 0) = cp - sp2;
+                        BB(0, C0 + q) = make_float2(cp + sp2, 0.f);
+                        BB(0, C0 - q) = make_float2(cp - sp2, 0.f);
                     }
                 } else {
                     cf A[KX + 1], D[KX + 1];
@@ -456,22 +530,20 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                         A[kx] = cadd(T[KX + kx], T[KX - kx]);
                         D[kx] = csub(T[KX + kx], T[KX - kx]);
                     }
-                    for (int q = 0; q <= c0; q++) {
-                        const int lx = c0 + q;
-                        const float g = t.s1g[lx];
+#pragma unroll
+                    for (int q = 0; q <= C0; q++) {
+                        const float g = t.s1g[C0 + q];
                         float cr = g * T[KX].r, ci = g * T[KX].i, sr = 0.f, si = 0.f;
 #pragma unroll
                         for (int kx = 1; kx <= KX; kx++) {
-                            const float c = t.s1c[lx][kx - 1], s = t.s1s[lx][kx - 1];
+                            const float c = t.s1c[C0 + q][kx - 1], s = t.s1s[C0 + q][kx - 1];
                             cr = fmaf(c, A[kx].r, cr);
                             ci = fmaf(c, A[kx].i, ci);
                             sr = fmaf(s, D[kx].i, sr);
                             si = fmaf(-s, D[kx].r, si);
                         }
-                        BB(r, c0 + q, 0) = cr + sr;
-                        BB(r, c0 + q, 1) = ci + si;
-                        BB(r, c0 - q, 0) = cr - sr;
-                        BB(r, c0 - q, 1) = ci - si;
+                        BB(r, C0 + q) = make_float2(cr + sr, ci + si);
+                        BB(r, C0 - q) = make_float2(cr - sr, ci - si);
                     }
                 }
             } else {
@@ -483,7 +555,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                             b = fmaf(2.f * t.s1c[lx][kx - 1], T[KX + kx].r, b);
                             b = fmaf(2.f * t.s1s[lx][kx - 1], T[KX + kx].i, b);
                         }
-                        BB(0, lx, 0) = b;
+                        BB(0, lx) = make_float2(b, 0.f);
                     }
                 } else {
                     cf A[KX + 1], D[KX + 1];
@@ -501,8 +573,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                             br = fmaf(c, A[kx].r, fmaf(s, D[kx].i, br));
                             bi = fmaf(c, A[kx].i, fmaf(-s, D[kx].r, bi));
                         }
-                        BB(r, lx, 0) = br;
-                        BB(r, lx, 1) = bi;
+                        BB(r, lx) = make_float2(br, bi);
                     }
                 }
             }
@@ -514,34 +585,43 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                 float best = -INFINITY;
                 int brk = 0x7fffffff;
                 for (int lx = r; lx < nlx; lx += NR) {
-                    const float b0 = BB(0, lx, 0);
+                    const float b0 = BB(0, lx).x;
                     float br[KY + 1], bi[KY + 1];
 #pragma unroll
                     for (int k = 1; k <= KY; k++) {
-                        br[k] = BB(k, lx, 0);
-                        bi[k] = BB(k, lx, 1);
+                        const float2 v = BB(k, lx);
+                        br[k] = v.x;
+                        bi[k] = v.y;
                     }
-                    if (t.sym_y) {
+                    if (NL && t.sym_y) {
                         // visit ly = 0, -1, +1, -2, +2, ...: ascending rank order within
-                        // a column (|v|^2 grows with |ly|, then iy ascending), so a
-                        // strict '>' keeps the reference's tie winner (_kernels.py:286-298)
-                        const int c0 = nly >> 1;
-                        float cb = t.s2g[c0] * b0;
+                        // a column (|v|^2 grows with |ly|, then iy ascending); two
+                        // interleaved chains (q odd / even) for ILP, each strict '>',
+                        // merged by visit index -> the reference's tie winner
+                        constexpr int C0 = NL / 2;
+                        float ca = -INFINITY, cb = t.s2g[C0] * b0;
 #pragma unroll
-                        for (int k = 1; k <= KY; k++) cb = fmaf(t.s2c[c0][k - 1], br[k], cb);
-                        int ci = c0;
-                        for (int q = 1; q <= c0; q++) {
-                            const int ly = c0 + q;
-                            float e = t.s2g[ly] * b0, o = 0.f;
+                        for (int k = 1; k <= KY; k++) cb = fmaf(t.s2c[C0][k - 1], br[k], cb);
+                        int ia = 0x7fff, ib = 0;
+#pragma unroll
+                        for (int q = 1; q <= C0; q++) {
+                            float e = t.s2g[C0 + q] * b0, o = 0.f;
 #pragma unroll
                             for (int k = 1; k <= KY; k++) {
-                                e = fmaf(t.s2c[ly][k - 1], br[k], e);
-                                o = fmaf(t.s2s[ly][k - 1], bi[k], o);
+                                e = fmaf(t.s2c[C0 + q][k - 1], br[k], e);
+                                o = fmaf(t.s2s[C0 + q][k - 1], bi[k], o);
                             }
                             const float vm = e - o, vp = e + o;
-                            if (vm > cb) { cb = vm; ci = c0 - q; }
-                            if (vp > cb) { cb = vp; ci = ly; }
+                            if (q & 1) {
+                                if (vm > ca) { ca = vm; ia = 2 * q - 1; }
+                                if (vp > ca) { ca = vp; ia = 2 * q; }
+                            } else {
+                                if (vm > cb) { cb = vm; ib = 2 * q - 1; }
+                                if (vp > cb) { cb = vp; ib = 2 * q; }
+                            }
                         }
+                        if (ca > cb || (ca == cb && ia < ib)) { cb = ca; ib = ia; }
+                        const int ci = (ib == 0) ? C0 : ((ib & 1) ? C0 - ((ib + 1) >> 1) : C0 + (ib >> 1));
                         const int rk = srank[ci * nlx + lx];
                         if (better(cb, rk, best, brk)) { best = cb; brk = rk; }
                     } else {
@@ -557,21 +637,24 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                         }
                     }
                 }
-                pbest[r * 32 + lane] = best;
-                prank[r * 32 + lane] = brk;
+                pbest[r * 32 + lane] = make_float2(best, __int_as_float(brk));
             }
-            __syncthreads();  // (4) partial maxima visible
+#undef BB
+            fence_proxy_async();  // stage reads before the next TMA write
+            __syncthreads();  // (4) partial maxima visible; the stage is free
+            if (yy + 1 < ye) issue(yy + 1, xb);
 
             // ---------------- phase E: final pick, PEF partial per row ----------------
             int vix, viy;
             {
-                float best = pbest[lane];
-                int brk = prank[lane];
+                const float2 bv = pbest[lane];
+                float best = bv.x;
+                int brk = __float_as_int(bv.y);
 #pragma unroll
                 for (int w = 1; w < NR; w++) {
-                    const float v = pbest[w * 32 + lane];
-                    const int rk = prank[w * 32 + lane];
-                    if (better(v, rk, best, brk)) { best = v; brk = rk; }
+                    const float2 o = pbest[w * 32 + lane];
+                    const int rk = __float_as_int(o.y);
+                    if (better(o.x, rk, best, brk)) { best = o.x; brk = rk; }
                 }
                 if (a.forced_ix >= 0) {
                     vix = a.forced_ix;
@@ -583,17 +666,24 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
             }
             if (r <= BY) {
                 // PEF on the retained band (_kernels.py:330-342), folded to the
-                // stored half space: pred = sum_j coef[v][j] * z+[j]
-                const float *cp = a.coefP + (size_t)(viy * nlx + vix) * G::NRET + G::prow(r);
-                const float *sr = sret + G::prow(r) * 32 + lane;
-                const int n = (r == 0) ? G::PROW0 : G::PROWN;
-                float acc0 = 0.f, acc1 = 0.f;
-#pragma unroll 10
-                for (int j = 0; j < n; j += 2) {
-                    acc0 = fmaf(__ldg(cp + j), sr[j * 32], acc0);
-                    if (j + 1 < n) acc1 = fmaf(__ldg(cp + j + 1), sr[(j + 1) * 32], acc1);
+                // stored half space: pred = sum_j coef[v][j] . z+[j]
+                const float2 *cp = a.coefP + (size_t)(viy * nlx + vix) * G::RETP + G::ppair(r);
+                const float2 *sr = sret + G::ppair(r) * 32 + lane;
+                float acc[4] = {0.f, 0.f, 0.f, 0.f};
+                if (r == 0) {
+#pragma unroll
+                    for (int j = 0; j < G::PROW0P; j++) {
+                        const float2 c = __ldg(cp + j), z = sr[j * 32];
+                        acc[j & 3] = fmaf(c.x, z.x, fmaf(c.y, z.y, acc[j & 3]));
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < G::PROWNP; j++) {
+                        const float2 c = __ldg(cp + j), z = sr[j * 32];
+                        acc[j & 3] = fmaf(c.x, z.x, fmaf(c.y, z.y, acc[j & 3]));
+                    }
                 }
-                ppef[r * 32 + lane] = acc0 + acc1;
+                ppef[r * 32 + lane] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
             }
             if (r == 0 && colv) {
                 uint8_t *vp = a.vidx + ((size_t)yy * W + x) * 2;
@@ -614,8 +704,6 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
         u += ye - ys;
     }
 #undef XFR
-#undef CXB
-#undef BB
 }
 
 }  // namespace cwb
