@@ -95,6 +95,9 @@ int cw_push_device(cw_handle *h, const float *frame_dev, int32_t *ready, int64_t
  * (H,W) f32, vidx (H,W,2) u8.  Valid until the next push. */
 int cw_device_outputs(cw_handle *h, float **residual, float **prediction, uint8_t **vidx);
 
+/* Synchronous device -> host copy (e.g. of cw_device_outputs buffers). */
+int cw_copy_to_host(cw_handle *h, void *dst, const void *src_dev, size_t bytes);
+
 /* Device pointer of the frame-ring slot the next push will use (for
  * producers that write frames in place, e.g. NCCL halo receives). */
 int cw_next_frame_slot(cw_handle *h, float **slot);

@@ -636,6 +636,14 @@ int cw_device_outputs(cw_handle *h, float **residual, float **prediction, uint8_
     return CW_OK;
 }
 
+int cw_copy_to_host(cw_handle *h, void *dst, const void *src_dev, size_t bytes)
+{
+    if (!h || !dst || !src_dev)
+        return CW_ERR_VALUE;
+    CW_CUDA(h, cudaMemcpy(dst, src_dev, bytes, cudaMemcpyDeviceToHost));
+    return CW_OK;
+}
+
 int cw_launch_info(const cw_handle *h, int32_t *kernels_per_push, int32_t *grid, int32_t *block,
                    int32_t *smem_bytes)
 {

@@ -186,18 +186,55 @@ class Pipeline:
         self.last_timings = {"pipeline": time.perf_counter() - t0}
         if not ready.value:
             return None
+        return self._wrap(int(fidx.value), res, pred, vidx)
+
+    def process_frame_device(self, frame) -> WhitenedOutput | None:
+        """``process_frame`` for a frame already in device memory: a CUDA
+        float32 (H, W) torch tensor on this pipeline's device (e.g. a strip
+        assembled from NCCL halo receives).  Runs on torch's current
+        stream; outputs are copied to fresh host arrays."""
+        import torch
+
+        if tuple(frame.shape) != (self.height, self.width) or frame.dtype != torch.float32 or not frame.is_cuda:
+            raise ValueError(f"expected a CUDA float32 tensor of shape {(self.height, self.width)}")
+        frame = frame.contiguous()
+        lib = _native.load()
+        t0 = time.perf_counter()
+        ready = ctypes.c_int32(0)
+        fidx = ctypes.c_int64(-1)
+        # run on a dedicated stream ordered after the producer of `frame`
+        # (handle 0 at the C ABI would mean the pipeline's own stream)
+        if getattr(self, "_tstream", None) is None:
+            self._tstream = torch.cuda.Stream(device=frame.device)
+        stream = self._tstream
+        stream.wait_stream(torch.cuda.current_stream(frame.device))
+        frame.record_stream(stream)
+        rc = lib.cw_push_device(self._h, ctypes.c_void_p(frame.data_ptr()), ctypes.byref(ready),
+                                ctypes.byref(fidx), ctypes.c_void_p(stream.cuda_stream))
+        _native.check(rc, self._h)
+        stream.synchronize()
+        if not ready.value:
+            self.last_timings = {"pipeline": time.perf_counter() - t0}
+            return None
+        res_p, pred_p, vidx_p = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+        _native.check(lib.cw_device_outputs(self._h, ctypes.byref(res_p), ctypes.byref(pred_p),
+                                            ctypes.byref(vidx_p)), self._h)
+        h, w = self.height, self.width
+        res = np.empty((h, w), np.float32)
+        pred = np.empty((h, w), np.float32)
+        vidx = np.empty((h, w, 2), np.uint8)
+        for dst, src in ((res, res_p), (pred, pred_p), (vidx, vidx_p)):
+            _native.check(lib.cw_copy_to_host(self._h, dst.ctypes.data, src, dst.nbytes), self._h)
+        self.last_timings = {"pipeline": time.perf_counter() - t0}
+        return self._wrap(int(fidx.value), res, pred, vidx)
+
+    def _wrap(self, frame_index, res, pred, vidx) -> WhitenedOutput:
         idx = vidx.astype(np.int32)
-        vel = np.empty((h, w, 2), np.float64)
+        vel = np.empty(idx.shape, np.float64)
         vel[..., 0] = self._lag_x[idx[..., 0]]
         vel[..., 1] = self._lag_y[idx[..., 1]]
-        return WhitenedOutput(
-            frame_index=int(fidx.value),
-            residual=res,
-            prediction=pred,
-            velocity=VelocityField(idx, vel),
-            mask=self.mask,
-            imag_peak=0.0,
-        )
+        return WhitenedOutput(frame_index=frame_index, residual=res, prediction=pred,
+                              velocity=VelocityField(idx, vel), mask=self.mask, imag_peak=0.0)
 
     # -- parity views (tests) ------------------------------------------------
 

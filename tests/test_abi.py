@@ -1,0 +1,72 @@
+"""The C ABI (include/cw_b200.h) on a CPU host: the sm_100a library loads,
+exports every declared entry point, and fails loudly (status code, no
+crash, no fallback) when asked for a device that is not there."""
+
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+from conftest import ROOT
+from paper_1408_3526_b200 import _native
+
+
+def _declared():
+    text = open(os.path.join(ROOT, "include", "cw_b200.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(cw_[a-z_0-9]+)\s*\(", text)))
+
+
+def test_header_and_binding_agree():
+    assert _declared() == sorted(_native.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _native.load()
+    out = subprocess.run(["nm", "-D", "--defined-only", _native.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (cw_\w+)", out))
+    for name in _declared():
+        assert name in exported, name
+        assert getattr(lib, name) is not None
+    assert lib.cw_abi_version() == 1
+
+
+def test_library_is_sm100a():
+    out = subprocess.run(["cuobjdump", "--list-elf", _native.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_create_without_device_reports_cuda_error(params, default_bank):
+    import numpy as np
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a CUDA device is present")
+    lib = _native.load()
+    cp, keep = _native.make_params(params)
+    coeffs = np.ascontiguousarray(default_bank.coeffs_flat, dtype=np.complex64)
+    ret = np.ascontiguousarray(default_bank.retained)
+    h = ctypes.c_void_p()
+    rc = lib.cw_create(ctypes.byref(cp), 64, 64, 0, _native.fptr(coeffs.view(np.float32)),
+                       ret.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), ret.size, 0, 0, ctypes.byref(h))
+    assert rc == _native.CW_ERR_CUDA and not h.value
+    assert b"cuda" in lib.cw_last_error(None).lower() or b"device" in lib.cw_last_error(None).lower()
+
+
+def test_create_rejects_bad_geometry_before_cuda(params, default_bank):
+    import numpy as np
+
+    lib = _native.load()
+    cp, keep = _native.make_params(params)
+    coeffs = np.ascontiguousarray(default_bank.coeffs_flat, dtype=np.complex64)
+    ret = np.ascontiguousarray(default_bank.retained)
+    h = ctypes.c_void_p()
+    rc = lib.cw_create(ctypes.byref(cp), 4, 4, 0, _native.fptr(coeffs.view(np.float32)),
+                       ret.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), ret.size, 0, 0, ctypes.byref(h))
+    assert rc == _native.CW_ERR_PARAM
+    assert b"smaller than analysis window" in lib.cw_last_error(None)
+    rc = lib.cw_create(ctypes.byref(cp), 64, 64, 0, _native.fptr(coeffs.view(np.float32)),
+                       ret.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), ret.size - 1, 0, 0, ctypes.byref(h))
+    assert rc == _native.CW_ERR_VALUE

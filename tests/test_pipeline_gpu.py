@@ -151,3 +151,92 @@ def test_outputs_are_fresh_copies(params):
                 keep.append((o, o.residual.copy()))
     for o, snap in keep:
         assert np.array_equal(o.residual, snap)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_strip_sharding_matches_full_frame(params, world):
+    """The per-rank strip pipelines (halo rows + row offset, strips.py) stitch
+    back to the full-frame result: emulated on one GPU by running every
+    rank's local strip in turn (the halo rows are the ones exchange_halo
+    delivers; the exchange itself is tested on gloo in test_strips_cpu)."""
+    import torch
+
+    from paper_1408_3526_b200 import Pipeline
+    from paper_1408_3526_b200.strips import plan_strips
+
+    rng = np.random.default_rng(world)
+    t, h, w = 9, 96, 70
+    frames = (10 + rng.standard_normal((t, h, w))).astype(np.float32)
+    full, _, _ = _run_gpu(params, frames)
+    plans = plan_strips(params, h, world)
+    res = np.zeros((len(full), h, w), np.float32)
+    idx = np.zeros((len(full), h, w, 2), np.int32)
+    for pl in plans:
+        with Pipeline(params, w, pl.local_height, _strip=(pl.halo, pl.lo)) as pipe:
+            k = 0
+            for n in range(t):
+                o = pipe.process_frame_device(torch.from_numpy(frames[n, pl.lo:pl.a1]).cuda())
+                if o is None:
+                    continue
+                mhy = params.mhat[1]
+                r0 = pl.halo - mhy if pl.halo else 0
+                res[k, pl.lo + r0: pl.a1 - mhy] = o.residual[r0: pl.local_height - mhy]
+                idx[k, pl.a0:pl.a1] = o.velocity.indices[pl.halo:]
+                k += 1
+            assert k == len(full)
+    fmax = float(np.abs(frames).max())
+    for k, g in enumerate(full):
+        assert velocity_agreement(idx[k], g.velocity.indices, params) >= VEL_FRAC
+        m = g.mask & agreeing_outputs(idx[k], g.velocity.indices, params)
+        assert residual_error(res[k], g.residual, m, fmax) <= RES_TOL
+
+
+def test_device_frame_entry_matches_host_entry(params):
+    import torch
+
+    from paper_1408_3526_b200 import Pipeline
+
+    rng = np.random.default_rng(3)
+    frames = (10 + rng.standard_normal((8, 40, 50))).astype(np.float32)
+    a, _, _ = _run_gpu(params, frames)
+    with Pipeline(params, 50, 40) as pipe:
+        b = [o for o in (pipe.process_frame_device(torch.from_numpy(f).cuda()) for f in frames) if o is not None]
+    for x, y in zip(a, b):
+        assert np.array_equal(x.residual, y.residual)
+        assert np.array_equal(x.velocity.indices, y.velocity.indices)
+
+
+def test_full_size_properties(params):
+    """640x512 (config C3 geometry): DC-offset invariance of the residual and
+    velocity agreement across offsets -- size-independent properties."""
+    from paper_1408_3526_b200.scenegen import SimConfig, generate
+
+    frames, _ = generate(SimConfig(width=640, height=512, frame_count=8, rng_seed=0))
+    a, _, _ = _run_gpu(params, frames)
+    b, _, _ = _run_gpu(params, frames + np.float32(5.0))
+    for x, y in zip(a, b):
+        m = x.mask & agreeing_outputs(x.velocity.indices, y.velocity.indices, params)
+        assert np.abs(x.residual[m] - y.residual[m]).max() <= 1e-3 * 5.0
+        assert velocity_agreement(x.velocity.indices, y.velocity.indices, params) >= 0.99
+
+
+def test_full_size_crop_parity_vs_oracle(params):
+    """640x512 C3 frames: the oracle on a 128x128 crop (plus the 8-px causal
+    margin) against the same crop of the full-frame GPU run."""
+    from paper_1408_3526_b200.scenegen import SimConfig, generate
+
+    frames, _ = generate(SimConfig(width=640, height=512, frame_count=10, rng_seed=0))
+    gpu, _, _ = _run_gpu(params, frames)
+    y0, x0, n = 200, 300, 128
+    crop = np.ascontiguousarray(frames[:, y0 - 8:y0 + n, x0 - 8:x0 + n])
+    ref = _run_oracle(params, crop)
+    fmax = float(np.abs(frames).max())
+    for g, r in zip(gpu, ref):
+        gi = g.velocity.indices[y0:y0 + n, x0:x0 + n]
+        ri = r["indices"][8:, 8:]
+        assert np.all(gi == ri, axis=-1).mean() >= VEL_FRAC
+        # outputs of the crop's anchors sit at anchor - mhat = (-4, -4)
+        same = np.all(gi == ri, axis=-1)
+        gres = g.residual[y0 - 4:y0 + n - 4, x0 - 4:x0 + n - 4]
+        rres = r["residual"][4:n + 4, 4:n + 4]
+        assert np.abs(gres - rres)[same].max() / fmax <= RES_TOL
