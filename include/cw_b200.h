@@ -95,6 +95,17 @@ int cw_push_device(cw_handle *h, const float *frame_dev, int32_t *ready, int64_t
  * (H,W) f32, vidx (H,W,2) u8.  Valid until the next push. */
 int cw_device_outputs(cw_handle *h, float **residual, float **prediction, uint8_t **vidx);
 
+/*
+ * Pipelined streaming: enqueue frame n's upload, kernel
+ * and result download on three streams and return at once; consecutive
+ * frames overlap (H2D of n+1 and D2H of n-1 run under kernel n).  Host
+ * buffers (pinned for true overlap) must stay valid until cw_wait(ticket)
+ * returns; at most 8 tickets may be outstanding.
+ */
+int cw_submit(cw_handle *h, const float *frame, float *residual, float *prediction, uint8_t *vidx,
+              int64_t *ticket);
+int cw_wait(cw_handle *h, int64_t ticket, int32_t *ready, int64_t *frame_index);
+
 /* Synchronous device -> host copy (e.g. of cw_device_outputs buffers). */
 int cw_copy_to_host(cw_handle *h, void *dst, const void *src_dev, size_t bytes);
 

@@ -96,8 +96,15 @@ struct cw_handle {
     int grid;
     cudaStream_t own = nullptr;
     float *d_state = nullptr, *d_that = nullptr, *d_coef = nullptr, *d_frames = nullptr;
-    float *d_res = nullptr, *d_pred = nullptr, *d_dbg = nullptr;
+    float *d_res = nullptr, *d_pred = nullptr, *d_dbg = nullptr;  // 2 output sets each
     uint8_t *d_vidx = nullptr;
+    int nslots = 0;  // frame ring slots: mhat_z + 2 (one spare for the async upload)
+    // async submit/wait (cw_submit): upload / download streams and per-frame events
+    cudaStream_t up = nullptr, down = nullptr;
+    static constexpr int NEV = 8;
+    cudaEvent_t ev_up[NEV] = {}, ev_k[NEV] = {}, ev_down[NEV] = {};
+    int ready_of[NEV] = {};
+    long long fidx_of[NEV] = {};
     size_t state_floats = 0, that_floats = 0;  // floats (pairs x 2)
     long long frames_seen = 0;
     bool have_that = false;
@@ -432,16 +439,25 @@ int cw_create(const cw_params *p, int32_t width, int32_t height, int32_t device,
     if (cudaMalloc(&h->d_state, h->state_floats * 4) != cudaSuccess ||
         cudaMalloc(&h->d_that, h->that_floats * 4) != cudaSuccess ||
         cudaMalloc(&h->d_coef, coef.size() * 4) != cudaSuccess ||
-        cudaMalloc(&h->d_frames, HW * 4 * (h->mhz + 1)) != cudaSuccess ||
-        cudaMalloc(&h->d_res, HW * 4) != cudaSuccess || cudaMalloc(&h->d_pred, HW * 4) != cudaSuccess ||
-        cudaMalloc(&h->d_vidx, HW * 2) != cudaSuccess)
+        cudaMalloc(&h->d_frames, HW * 4 * (h->mhz + 2)) != cudaSuccess ||
+        cudaMalloc(&h->d_res, HW * 4 * 2) != cudaSuccess || cudaMalloc(&h->d_pred, HW * 4 * 2) != cudaSuccess ||
+        cudaMalloc(&h->d_vidx, HW * 2 * 2) != cudaSuccess)
         return cleanup_fail(CW_ERR_NOMEM, "device allocation failed");
     cudaMemsetAsync(h->d_state, 0, h->state_floats * 4, h->own);
     cudaMemsetAsync(h->d_that, 0, h->that_floats * 4, h->own);
-    cudaMemsetAsync(h->d_frames, 0, HW * 4 * (h->mhz + 1), h->own);
-    cudaMemsetAsync(h->d_res, 0, HW * 4, h->own);
-    cudaMemsetAsync(h->d_pred, 0, HW * 4, h->own);
-    cudaMemsetAsync(h->d_vidx, 0, HW * 2, h->own);
+    h->nslots = h->mhz + 2;
+    cudaMemsetAsync(h->d_frames, 0, HW * 4 * h->nslots, h->own);
+    cudaMemsetAsync(h->d_res, 0, HW * 4 * 2, h->own);
+    cudaMemsetAsync(h->d_pred, 0, HW * 4 * 2, h->own);
+    cudaMemsetAsync(h->d_vidx, 0, HW * 2 * 2, h->own);
+    if (cudaStreamCreateWithFlags(&h->up, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&h->down, cudaStreamNonBlocking) != cudaSuccess)
+        return cleanup_fail(CW_ERR_CUDA, "cudaStreamCreate failed");
+    for (int i = 0; i < cw_handle::NEV; i++)
+        if (cudaEventCreateWithFlags(&h->ev_up[i], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&h->ev_k[i], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&h->ev_down[i], cudaEventDisableTiming) != cudaSuccess)
+            return cleanup_fail(CW_ERR_CUDA, "cudaEventCreate failed");
     cudaMemcpyAsync(h->d_coef, coef.data(), coef.size() * 4, cudaMemcpyHostToDevice, h->own);
     if (cudaStreamSynchronize(h->own) != cudaSuccess)
         return cleanup_fail(CW_ERR_CUDA, "device initialisation failed");
@@ -465,6 +481,19 @@ void cw_destroy(cw_handle *h)
     cudaFree(h->d_dbg);
     for (cudaEvent_t e : h->ev_pool)
         cudaEventDestroy(e);
+    for (int i = 0; i < cw_handle::NEV; i++) {
+        if (h->ev_up[i]) cudaEventDestroy(h->ev_up[i]);
+        if (h->ev_k[i]) cudaEventDestroy(h->ev_k[i]);
+        if (h->ev_down[i]) cudaEventDestroy(h->ev_down[i]);
+    }
+    if (h->up) {
+        cudaStreamSynchronize(h->up);
+        cudaStreamDestroy(h->up);
+    }
+    if (h->down) {
+        cudaStreamSynchronize(h->down);
+        cudaStreamDestroy(h->down);
+    }
     if (h->own)
         cudaStreamDestroy(h->own);
     delete h;
@@ -505,7 +534,7 @@ int cw_next_frame_slot(cw_handle *h, float **slot)
     if (!h || !slot)
         return CW_ERR_VALUE;
     const size_t HW = (size_t)h->W * h->H;
-    *slot = h->d_frames + (size_t)(h->frames_seen % (h->mhz + 1)) * HW;
+    *slot = h->d_frames + (size_t)(h->frames_seen % h->nslots) * HW;
     return CW_OK;
 }
 
@@ -521,14 +550,15 @@ static int run_frame(cw_handle *h, cudaStream_t s, int32_t *ready, int64_t *fram
     const long long n = h->frames_seen;
     const int rd = (n + 1 >= h->mz) ? 1 : 0;
     FrameArgs a;
-    a.frame = h->d_frames + (size_t)(n % (h->mhz + 1)) * HW;
-    a.delayed = rd ? h->d_frames + (size_t)(((n - h->mhz) % (h->mhz + 1))) * HW : nullptr;
+    a.frame = h->d_frames + (size_t)(n % h->nslots) * HW;
+    a.delayed = rd ? h->d_frames + (size_t)((n - h->mhz) % h->nslots) * HW : nullptr;
     a.state = reinterpret_cast<float2 *>(h->d_state);
     a.that = reinterpret_cast<float2 *>(h->d_that);
     a.coefP = reinterpret_cast<const float2 *>(h->d_coef);
-    a.res = h->d_res;
-    a.pred = h->d_pred;
-    a.vidx = h->d_vidx;
+    const size_t set = (size_t)(n & 1);  // double-buffered outputs
+    a.res = h->d_res + set * HW;
+    a.pred = h->d_pred + set * HW;
+    a.vidx = h->d_vidx + set * HW * 2;
     a.dbgS = h->debug ? reinterpret_cast<float2 *>(h->d_dbg) : nullptr;
     a.W = h->W;
     a.H = h->H;
@@ -598,6 +628,7 @@ int cw_push(cw_handle *h, const float *frame, float *residual, float *prediction
     const size_t HW = (size_t)h->W * h->H;
     CW_CUDA(h, cudaMemcpyAsync(slot, frame, HW * 4, cudaMemcpyHostToDevice, s));
     int32_t rd = 0;
+    const size_t set = (size_t)(h->frames_seen & 1);
     int rc = run_frame(h, s, &rd, frame_index);
     if (rc != CW_OK)
         return rc;
@@ -606,15 +637,15 @@ int cw_push(cw_handle *h, const float *frame, float *residual, float *prediction
     bool sync = false;
     if (rd) {
         if (residual) {
-            CW_CUDA(h, cudaMemcpyAsync(residual, h->d_res, HW * 4, cudaMemcpyDeviceToHost, s));
+            CW_CUDA(h, cudaMemcpyAsync(residual, h->d_res + set * HW, HW * 4, cudaMemcpyDeviceToHost, s));
             sync = true;
         }
         if (prediction) {
-            CW_CUDA(h, cudaMemcpyAsync(prediction, h->d_pred, HW * 4, cudaMemcpyDeviceToHost, s));
+            CW_CUDA(h, cudaMemcpyAsync(prediction, h->d_pred + set * HW, HW * 4, cudaMemcpyDeviceToHost, s));
             sync = true;
         }
         if (vidx) {
-            CW_CUDA(h, cudaMemcpyAsync(vidx, h->d_vidx, HW * 2, cudaMemcpyDeviceToHost, s));
+            CW_CUDA(h, cudaMemcpyAsync(vidx, h->d_vidx + set * HW * 2, HW * 2, cudaMemcpyDeviceToHost, s));
             sync = true;
         }
     }
@@ -627,12 +658,74 @@ int cw_device_outputs(cw_handle *h, float **residual, float **prediction, uint8_
 {
     if (!h)
         return CW_ERR_VALUE;
+    const size_t HW = (size_t)h->W * h->H;
+    const size_t set = (size_t)((h->frames_seen + 1) & 1);  // set of the latest pushed frame
     if (residual)
-        *residual = h->d_res;
+        *residual = h->d_res + set * HW;
     if (prediction)
-        *prediction = h->d_pred;
+        *prediction = h->d_pred + set * HW;
     if (vidx)
-        *vidx = h->d_vidx;
+        *vidx = h->d_vidx + set * HW * 2;
+    return CW_OK;
+}
+
+// Asynchronous pipelined push: upload (stream `up`), frame kernel (own
+// stream) and download (stream `down`) of consecutive frames overlap.
+//  H2D(n) into slot n % (mhat_z+2) waits for kernel(n-2), the last reader
+//  of that slot (as the delayed frame of n-2 ... or current frame n-R);
+//  kernel(n) waits for H2D(n) and for D2H(n-2), which read output set n % 2;
+//  D2H(n) waits for kernel(n).  Host buffers should be pinned.
+int cw_submit(cw_handle *h, const float *frame, float *residual, float *prediction, uint8_t *vidx,
+              int64_t *ticket)
+{
+    if (!h || !frame || !ticket)
+        return CW_ERR_VALUE;
+    const size_t HW = (size_t)h->W * h->H;
+    const long long n = h->frames_seen;
+    const int e = (int)(n % cw_handle::NEV);
+    if (n >= cw_handle::NEV)  // ticket n - NEV must have been collected
+        CW_CUDA(h, cudaEventSynchronize(h->ev_down[e]));
+    if (n >= 2)
+        CW_CUDA(h, cudaStreamWaitEvent(h->up, h->ev_k[(n - 2) % cw_handle::NEV], 0));
+    float *slot = h->d_frames + (size_t)(n % h->nslots) * HW;
+    CW_CUDA(h, cudaMemcpyAsync(slot, frame, HW * 4, cudaMemcpyHostToDevice, h->up));
+    CW_CUDA(h, cudaEventRecord(h->ev_up[e], h->up));
+    CW_CUDA(h, cudaStreamWaitEvent(h->own, h->ev_up[e], 0));
+    if (n >= 2)
+        CW_CUDA(h, cudaStreamWaitEvent(h->own, h->ev_down[(n - 2) % cw_handle::NEV], 0));
+    int32_t rd = 0;
+    int64_t fi = -1;
+    const size_t set = (size_t)(n & 1);
+    int rc = run_frame(h, h->own, &rd, &fi);
+    if (rc != CW_OK)
+        return rc;
+    CW_CUDA(h, cudaEventRecord(h->ev_k[e], h->own));
+    CW_CUDA(h, cudaStreamWaitEvent(h->down, h->ev_k[e], 0));
+    if (rd) {
+        if (residual)
+            CW_CUDA(h, cudaMemcpyAsync(residual, h->d_res + set * HW, HW * 4, cudaMemcpyDeviceToHost, h->down));
+        if (prediction)
+            CW_CUDA(h, cudaMemcpyAsync(prediction, h->d_pred + set * HW, HW * 4, cudaMemcpyDeviceToHost, h->down));
+        if (vidx)
+            CW_CUDA(h, cudaMemcpyAsync(vidx, h->d_vidx + set * HW * 2, HW * 2, cudaMemcpyDeviceToHost, h->down));
+    }
+    CW_CUDA(h, cudaEventRecord(h->ev_down[e], h->down));
+    h->ready_of[e] = rd;
+    h->fidx_of[e] = fi;
+    *ticket = n;
+    return CW_OK;
+}
+
+int cw_wait(cw_handle *h, int64_t ticket, int32_t *ready, int64_t *frame_index)
+{
+    if (!h || ticket < 0 || ticket >= h->frames_seen || ticket < h->frames_seen - cw_handle::NEV)
+        return h ? fail(h, CW_ERR_VALUE, "unknown or expired ticket") : CW_ERR_VALUE;
+    const int e = (int)(ticket % cw_handle::NEV);
+    CW_CUDA(h, cudaEventSynchronize(h->ev_down[e]));
+    if (ready)
+        *ready = h->ready_of[e];
+    if (frame_index)
+        *frame_index = h->fidx_of[e];
     return CW_OK;
 }
 

@@ -19,7 +19,9 @@ Differences from the reference, by design:
 from __future__ import annotations
 
 import ctypes
+import threading
 import time
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -61,6 +63,68 @@ def apply_pef(bins, kernel, delayed_intensity: float):
     band = bins[:, cy - hy : cy + hy + 1, cx - hx : cx + hx + 1]
     pred = float(np.sum(coeffs.astype(np.complex128) * band).real)
     return pred, float(delayed_intensity) - pred
+
+
+class _LazyVelocityField(VelocityField):
+    """VelocityField whose int32 ``indices`` and float64 ``velocities``
+    (flow.py:134-144) are expanded from the device's uint8 (ix, iy) pairs on
+    first access, through 64K-entry lookup tables."""
+
+    def __init__(self, codes, lut_i, lut_v):
+        self._codes, self._lut_i, self._lut_v = codes, lut_i, lut_v
+        self._i = self._v = None
+
+    @property
+    def indices(self):
+        if self._i is None:
+            self._i = self._lut_i[self._codes]
+        return self._i
+
+    @indices.setter
+    def indices(self, value):
+        self._i = value
+
+    @property
+    def velocities(self):
+        if self._v is None:
+            self._v = self._lut_v[self._codes]
+        return self._v
+
+    @velocities.setter
+    def velocities(self, value):
+        self._v = value
+
+
+class _PinnedPool:
+    """Recycled page-locked host buffers for per-call output arrays.
+
+    Every ``process_frame`` returns fresh arrays (the reference copies its
+    outputs, pipeline.py:288-292); backing them with pinned memory lets the
+    device copy them at full PCIe rate.  A buffer goes back to the pool when
+    the array handed out (and every view of it) has been garbage collected.
+    """
+
+    def __init__(self):
+        self._free: dict[tuple, list] = {}
+        self._lock = threading.Lock()
+
+    def take(self, shape, dtype):
+        import torch
+
+        key = (tuple(shape), np.dtype(dtype).str)
+        with self._lock:
+            stack = self._free.setdefault(key, [])
+            tensor = stack.pop() if stack else None
+        if tensor is None:
+            tdt = {np.dtype(np.float32): torch.float32, np.dtype(np.uint8): torch.uint8}[np.dtype(dtype)]
+            tensor = torch.empty(shape, dtype=tdt, pin_memory=True)
+        arr = tensor.numpy()
+        weakref.finalize(arr, self._give, key, tensor)
+        return arr
+
+    def _give(self, key, tensor):
+        with self._lock:
+            self._free.setdefault(key, []).append(tensor)
 
 
 @dataclass
@@ -121,6 +185,12 @@ class Pipeline:
         self.last_timings: dict[str, float] = {}
         self._lag_x = np.asarray(params.lag_grid_x, dtype=np.float64)
         self._lag_y = np.asarray(params.lag_grid_y, dtype=np.float64)
+        # (ix | iy << 8) -> (ix, iy) int32 and (vx, vy) float64
+        code = np.arange(65536)
+        ix, iy = np.minimum(code & 255, len(self._lag_x) - 1), np.minimum(code >> 8, len(self._lag_y) - 1)
+        self._lut_i = np.stack([code & 255, code >> 8], axis=-1).astype(np.int32)
+        self._lut_v = np.stack([self._lag_x[ix], self._lag_y[iy]], axis=-1)
+        self._pool = _PinnedPool()
 
         self._forced = None
         if forced_velocity is not None:
@@ -172,9 +242,9 @@ class Pipeline:
         lib = _native.load()
         t0 = time.perf_counter()
         h, w = self.height, self.width
-        res = np.empty((h, w), np.float32)
-        pred = np.empty((h, w), np.float32)
-        vidx = np.empty((h, w, 2), np.uint8)
+        res = self._pool.take((h, w), np.float32)
+        pred = self._pool.take((h, w), np.float32)
+        vidx = self._pool.take((h, w, 2), np.uint8)
         ready = ctypes.c_int32(0)
         fidx = ctypes.c_int64(-1)
         rc = lib.cw_push(
@@ -187,6 +257,50 @@ class Pipeline:
         if not ready.value:
             return None
         return self._wrap(int(fidx.value), res, pred, vidx)
+
+    def process_stream(self, frames, depth: int = 3):
+        """Pipelined ``process_frame`` over an iterable of (H, W) frames.
+
+        Yields the same WhitenedOutput sequence as calling ``process_frame``
+        on each frame (warm-up frames yield nothing), but keeps up to
+        ``depth`` frames in flight so that the upload of frame n+1 and the
+        download of frame n-1 overlap the kernel of frame n (cw_submit /
+        cw_wait).  Pinned input frames (e.g. numpy views
+        of ``torch.empty(..., pin_memory=True)``) give fully async uploads.
+        """
+        from collections import deque
+
+        lib = _native.load()
+        depth = max(1, min(int(depth), 6))
+        h, w = self.height, self.width
+        inflight: deque = deque()
+
+        def collect(item):
+            ticket, _frame, res, pred, vidx = item
+            ready, fidx = ctypes.c_int32(0), ctypes.c_int64(-1)
+            _native.check(lib.cw_wait(self._h, ticket, ctypes.byref(ready), ctypes.byref(fidx)), self._h)
+            return self._wrap(int(fidx.value), res, pred, vidx) if ready.value else None
+
+        for frame in frames:
+            frame = np.ascontiguousarray(frame, dtype=np.float32)
+            if frame.shape != (h, w):
+                raise ValueError(f"frame shape {frame.shape} != {(h, w)}")
+            res = self._pool.take((h, w), np.float32)
+            pred = self._pool.take((h, w), np.float32)
+            vidx = self._pool.take((h, w, 2), np.uint8)
+            ticket = ctypes.c_int64(-1)
+            rc = lib.cw_submit(self._h, _native.fptr(frame), _native.fptr(res), _native.fptr(pred),
+                               vidx.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), ctypes.byref(ticket))
+            _native.check(rc, self._h)
+            inflight.append((ticket.value, frame, res, pred, vidx))
+            while len(inflight) > depth:
+                out = collect(inflight.popleft())
+                if out is not None:
+                    yield out
+        while inflight:
+            out = collect(inflight.popleft())
+            if out is not None:
+                yield out
 
     def process_frame_device(self, frame) -> WhitenedOutput | None:
         """``process_frame`` for a frame already in device memory: a CUDA
@@ -229,12 +343,10 @@ class Pipeline:
         return self._wrap(int(fidx.value), res, pred, vidx)
 
     def _wrap(self, frame_index, res, pred, vidx) -> WhitenedOutput:
-        idx = vidx.astype(np.int32)
-        vel = np.empty(idx.shape, np.float64)
-        vel[..., 0] = self._lag_x[idx[..., 0]]
-        vel[..., 1] = self._lag_y[idx[..., 1]]
+        codes = vidx.view(np.uint16).reshape(vidx.shape[:2])
         return WhitenedOutput(frame_index=frame_index, residual=res, prediction=pred,
-                              velocity=VelocityField(idx, vel), mask=self.mask, imag_peak=0.0)
+                              velocity=_LazyVelocityField(codes, self._lut_i, self._lut_v),
+                              mask=self.mask, imag_peak=0.0)
 
     # -- parity views (tests) ------------------------------------------------
 

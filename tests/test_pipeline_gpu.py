@@ -240,3 +240,40 @@ def test_full_size_crop_parity_vs_oracle(params):
         gres = g.residual[y0 - 4:y0 + n - 4, x0 - 4:x0 + n - 4]
         rres = r["residual"][4:n + 4, 4:n + 4]
         assert np.abs(gres - rres)[same].max() / fmax <= RES_TOL
+
+
+def test_process_stream_matches_process_frame(params):
+    """The pipelined stream API (cw_submit/cw_wait, three streams) gives the
+    same outputs as the synchronous call, frame for frame."""
+    import torch
+
+    from paper_1408_3526_b200 import Pipeline
+
+    rng = np.random.default_rng(11)
+    frames = (10 + rng.standard_normal((14, 48, 70))).astype(np.float32)
+    pinned = torch.empty(frames.shape, dtype=torch.float32, pin_memory=True)
+    pinned.copy_(torch.from_numpy(frames))
+    a, _, _ = _run_gpu(params, frames)
+    for depth in (1, 3, 6):
+        with Pipeline(params, 70, 48) as pipe:
+            b = list(pipe.process_stream(pinned.numpy(), depth=depth))
+        assert [o.frame_index for o in b] == [o.frame_index for o in a]
+        for x, y in zip(a, b):
+            assert np.array_equal(x.residual, y.residual)
+            assert np.array_equal(x.prediction, y.prediction)
+            assert np.array_equal(x.velocity.indices, y.velocity.indices)
+            assert np.array_equal(x.velocity.velocities, y.velocity.velocities)
+
+
+def test_lazy_velocity_field_contract(params):
+    """WhitenedOutput.velocity keeps the reference types (flow.py:134-144):
+    int32 (H, W, 2) indices and float64 (H, W, 2) velocities = lag values."""
+    rng = np.random.default_rng(12)
+    frames = (10 + rng.standard_normal((7, 20, 24))).astype(np.float32)
+    gpu, _, _ = _run_gpu(params, frames)
+    v = gpu[-1].velocity
+    assert v.indices.dtype == np.int32 and v.indices.shape == (20, 24, 2)
+    assert v.velocities.dtype == np.float64 and v.velocities.shape == (20, 24, 2)
+    lag = np.asarray(params.lag_grid_x)
+    assert np.array_equal(v.velocities[..., 0], lag[v.indices[..., 0]])
+    assert np.array_equal(v.velocities[..., 1], lag[v.indices[..., 1]])
