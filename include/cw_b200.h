@@ -106,6 +106,21 @@ int cw_submit(cw_handle *h, const float *frame, float *residual, float *predicti
               int64_t *ticket);
 int cw_wait(cw_handle *h, int64_t ticket, int32_t *ready, int64_t *frame_index);
 
+/*
+ * Fused detection epilogue ("final threshold"; the truth-free
+ * metrics of cli.compute_metrics_row, cli.py:157-208).  cw_set_detection(h,
+ * tau, cap): every valid output pixel with |residual| >= tau (tau <= 0: no
+ * list) is appended (x, y, residual) to a per-frame list of capacity `cap`
+ * (cap < 0 turns the epilogue off).  cw_detections(h, ticket, ...) for a
+ * completed frame (ticket = cw_submit ticket, or the frame number n of a
+ * synchronising push): *n_total = detections found (may exceed cap),
+ * xyr = up to out_cap (x, y, residual) triples in arbitrary order, stats =
+ * {peak |res|, peak x, peak y (first in row-major order on ties),
+ *  sum res^2, n valid outputs}.
+ */
+int cw_set_detection(cw_handle *h, float tau, int32_t cap);
+int cw_detections(cw_handle *h, int64_t ticket, int32_t *n_total, float *xyr, int32_t out_cap, double *stats);
+
 /* Synchronous device -> host copy (e.g. of cw_device_outputs buffers). */
 int cw_copy_to_host(cw_handle *h, void *dst, const void *src_dev, size_t bytes);
 

@@ -105,6 +105,13 @@ struct cw_handle {
     cudaEvent_t ev_up[NEV] = {}, ev_k[NEV] = {}, ev_down[NEV] = {};
     int ready_of[NEV] = {};
     long long fidx_of[NEV] = {};
+    // detection epilogue: 2 device sets (double-buffered like the outputs),
+    // NEV pinned host mirrors (one per outstanding frame)
+    float det_tau = 0.f;
+    int det_cap = 0;
+    bool det_on = false;
+    unsigned char *d_det = nullptr, *h_det = nullptr;
+    size_t det_bytes = 0;
     size_t state_floats = 0, that_floats = 0;  // floats (pairs x 2)
     long long frames_seen = 0;
     bool have_that = false;
@@ -479,6 +486,9 @@ void cw_destroy(cw_handle *h)
     cudaFree(h->d_pred);
     cudaFree(h->d_vidx);
     cudaFree(h->d_dbg);
+    cudaFree(h->d_det);
+    if (h->h_det)
+        cudaFreeHost(h->h_det);
     for (cudaEvent_t e : h->ev_pool)
         cudaEventDestroy(e);
     for (int i = 0; i < cw_handle::NEV; i++) {
@@ -571,6 +581,13 @@ static int run_frame(cw_handle *h, cudaStream_t s, int32_t *ready, int64_t *fram
     a.forced_iy = h->forced_iy;
     a.mhx = h->mhx;
     a.mhy = h->mhy;
+    a.det = nullptr;
+    a.det_tau = h->det_tau;
+    a.det_cap = h->det_cap;
+    if (h->det_on && rd) {
+        a.det = h->d_det + set * h->det_bytes;
+        CW_CUDA(h, cudaMemsetAsync(a.det, 0, 64, s));
+    }
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (h->timing) {
         while (h->ev_pool.size() < h->ev_used + 2) {
@@ -587,6 +604,10 @@ static int run_frame(cw_handle *h, cudaStream_t s, int32_t *ready, int64_t *fram
     CW_CUDA(h, cudaGetLastError());
     if (h->timing)
         CW_CUDA(h, cudaEventRecord(e1, s));
+    if (a.det) {  // results to the pinned mirror of this frame (ordered on s)
+        CW_CUDA(h, cudaMemcpyAsync(h->h_det + (size_t)(n % cw_handle::NEV) * h->det_bytes, a.det,
+                                   64 + (size_t)h->det_cap * 16, cudaMemcpyDeviceToHost, s));
+    }
     h->frames_seen = n + 1;
     if (rd)
         h->have_that = true;
@@ -726,6 +747,70 @@ int cw_wait(cw_handle *h, int64_t ticket, int32_t *ready, int64_t *frame_index)
         *ready = h->ready_of[e];
     if (frame_index)
         *frame_index = h->fidx_of[e];
+    return CW_OK;
+}
+
+int cw_set_detection(cw_handle *h, float tau, int32_t cap)
+{
+    if (!h)
+        return CW_ERR_VALUE;
+    if (cap < 0) {  // off
+        h->det_on = false;
+        return CW_OK;
+    }
+    const size_t bytes = 64 + (size_t)cap * 16;
+    if (bytes != h->det_bytes) {
+        CW_CUDA(h, cudaSetDevice(h->device));
+        CW_CUDA(h, cudaDeviceSynchronize());
+        cudaFree(h->d_det);
+        if (h->h_det)
+            cudaFreeHost(h->h_det);
+        h->d_det = nullptr;
+        h->h_det = nullptr;
+        CW_CUDA(h, cudaMalloc(&h->d_det, 2 * bytes));
+        CW_CUDA(h, cudaMallocHost(&h->h_det, cw_handle::NEV * bytes));
+        std::memset(h->h_det, 0, cw_handle::NEV * bytes);
+        h->det_bytes = bytes;
+    }
+    h->det_tau = tau;
+    h->det_cap = cap;
+    h->det_on = true;
+    return CW_OK;
+}
+
+int cw_detections(cw_handle *h, int64_t ticket, int32_t *n_total, float *xyr, int32_t out_cap, double *stats)
+{
+    if (!h || !h->det_on || ticket < 0 || ticket >= h->frames_seen || ticket < h->frames_seen - cw_handle::NEV)
+        return h ? fail(h, CW_ERR_VALUE, "detections unavailable for this frame") : CW_ERR_VALUE;
+    const unsigned char *b = h->h_det + (size_t)(ticket % cw_handle::NEV) * h->det_bytes;
+    unsigned int count;
+    unsigned long long key, nval;
+    double sumsq;
+    std::memcpy(&count, b, 4);
+    std::memcpy(&key, b + 8, 8);
+    std::memcpy(&sumsq, b + 16, 8);
+    std::memcpy(&nval, b + 24, 8);
+    if (n_total)
+        *n_total = (int32_t)count;
+    const int k = (int)std::min<long long>(std::min<long long>(count, h->det_cap), std::max(0, out_cap));
+    for (int i = 0; i < k && xyr; i++) {
+        float v[4];
+        std::memcpy(v, b + 64 + (size_t)i * 16, 16);
+        xyr[3 * i] = v[0];
+        xyr[3 * i + 1] = v[1];
+        xyr[3 * i + 2] = v[2];
+    }
+    if (stats) {
+        unsigned int bits = (unsigned int)(key >> 32);
+        float peak;
+        std::memcpy(&peak, &bits, 4);
+        const unsigned long long idx = 0xffffffffull - (key & 0xffffffffull);
+        stats[0] = nval ? peak : 0.0;
+        stats[1] = nval ? (double)(idx % h->W) : -1.0;
+        stats[2] = nval ? (double)(idx / h->W) : -1.0;
+        stats[3] = sumsq;
+        stats[4] = (double)nval;
+    }
     return CW_OK;
 }
 

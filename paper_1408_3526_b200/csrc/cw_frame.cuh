@@ -80,7 +80,46 @@ struct FrameArgs {
     int ready, first;      // flow/PEF enabled; first ready frame (T^ := T)
     int forced_ix, forced_iy;  // < 0: no override
     int mhx, mhy;
+    // detection epilogue (nullable): header {u32 count; u64 peak key;
+    // f64 sum res^2; u64 n valid} then float4 (x, y, res, 0) x det_cap
+    unsigned char *det;
+    float det_tau;  // |res| >= det_tau is a detection (<= 0: list off)
+    int det_cap;
 };
+
+// Fused "final threshold" and the ground-truth-free metrics of
+// cli.compute_metrics_row (cli.py:157-208): detections |res| >= tau, the peak
+// |res| (ties -> first pixel in row-major order, as np.argmax) and sum res^2
+// over the valid outputs.  One warp (the residual lanes of a CTA row).
+__device__ __forceinline__ void detect_epilogue(const FrameArgs &a, bool valid, int ox, int oy, float res)
+{
+    unsigned int *count = reinterpret_cast<unsigned int *>(a.det);
+    unsigned long long *peak = reinterpret_cast<unsigned long long *>(a.det + 8);
+    double *sumsq = reinterpret_cast<double *>(a.det + 16);
+    unsigned long long *nval = reinterpret_cast<unsigned long long *>(a.det + 24);
+    float4 *list = reinterpret_cast<float4 *>(a.det + 64);
+    const float v = fabsf(res);
+    if (valid && a.det_tau > 0.f && v >= a.det_tau) {
+        const unsigned int slot = atomicAdd(count, 1u);
+        if (slot < (unsigned int)a.det_cap) list[slot] = make_float4((float)ox, (float)oy, res, 0.f);
+    }
+    unsigned long long key =
+        valid ? ((unsigned long long)__float_as_uint(v) << 32) | (0xffffffffull - (unsigned long long)((size_t)oy * a.W + ox))
+              : 0ull;
+    float sq = valid ? res * res : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long k2 = __shfl_xor_sync(0xffffffffu, key, o);
+        key = k2 > key ? k2 : key;
+        sq += __shfl_xor_sync(0xffffffffu, sq, o);
+    }
+    const unsigned int nv = __popc(__ballot_sync(0xffffffffu, valid));
+    if ((threadIdx.x & 31) == 0 && nv) {
+        atomicMax(peak, key);
+        atomicAdd(sumsq, (double)sq);
+        atomicAdd(nval, (unsigned long long)nv);
+    }
+}
 
 template <int KX_, int KY_, int KZ_, int BX_, int BY_>
 struct Geo {
@@ -691,14 +730,19 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
             }
             __syncthreads();  // (5) PEF partials visible
 
-            // ---------------- phase F: residual ----------------
-            if (r == 0 && anchor) {
-                float p = 0.f;
+            // ---------------- phase F: residual (+ threshold epilogue) ----------------
+            if (r == 0) {
+                float rv = 0.f;
+                if (anchor) {
+                    float p = 0.f;
 #pragma unroll
-                for (int k = 0; k <= BY; k++) p += ppef[k * 32 + lane];
-                const size_t o = (size_t)(yy - a.mhy) * W + (x - a.mhx);
-                a.res[o] = __ldg(a.delayed + o) - p;
-                if (a.pred) a.pred[o] = p;
+                    for (int k = 0; k <= BY; k++) p += ppef[k * 32 + lane];
+                    const size_t o = (size_t)(yy - a.mhy) * W + (x - a.mhx);
+                    rv = __ldg(a.delayed + o) - p;
+                    a.res[o] = rv;
+                    if (a.pred) a.pred[o] = p;
+                }
+                if (a.det) detect_epilogue(a, anchor, x - a.mhx, yy - a.mhy, rv);
             }
         }
         u += ye - ys;

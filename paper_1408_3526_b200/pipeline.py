@@ -129,7 +129,14 @@ class _PinnedPool:
 
 @dataclass
 class WhitenedOutput:
-    """One whitened frame (pipeline.py:84-99)."""
+    """One whitened frame (pipeline.py:84-99).
+
+    ``detections`` / ``metrics`` are filled only when the pipeline was built
+    with ``detect_threshold`` (the fused final-threshold epilogue):
+    detections = (N, 3) float64 [x, y, residual] rows sorted by (y, x);
+    metrics = {peak_abs_residual, peak_x, peak_y, residual_rms, n_valid,
+    n_detections, truncated} (cli.compute_metrics_row without ground truth).
+    """
 
     frame_index: int
     residual: np.ndarray
@@ -137,6 +144,8 @@ class WhitenedOutput:
     velocity: VelocityField
     mask: np.ndarray
     imag_peak: float
+    detections: np.ndarray | None = None
+    metrics: dict | None = None
 
 
 class Pipeline:
@@ -156,6 +165,8 @@ class Pipeline:
         forced_velocity=None,
         bank: FilterBank | None = None,
         device: int = 0,
+        detect_threshold: float | None = None,
+        max_detections: int = 65536,
         _strip: tuple[int, int] = (0, 0),
     ):
         validate(params)
@@ -212,6 +223,10 @@ class Pipeline:
         self._h = handle
         if self._forced is not None:
             _native.check(lib.cw_set_forced_velocity(self._h, *self._forced), self._h)
+        self._detect = detect_threshold is not None
+        self._max_det = int(max_detections)
+        if self._detect:
+            _native.check(lib.cw_set_detection(self._h, float(detect_threshold), self._max_det), self._h)
 
     # -- reference properties (pipeline.py:179-199) -------------------------
 
@@ -256,7 +271,7 @@ class Pipeline:
         self.last_timings = {"pipeline": time.perf_counter() - t0}
         if not ready.value:
             return None
-        return self._wrap(int(fidx.value), res, pred, vidx)
+        return self._wrap(int(fidx.value), res, pred, vidx, ticket=self.frames_seen - 1)
 
     def process_stream(self, frames, depth: int = 3):
         """Pipelined ``process_frame`` over an iterable of (H, W) frames.
@@ -279,7 +294,7 @@ class Pipeline:
             ticket, _frame, res, pred, vidx = item
             ready, fidx = ctypes.c_int32(0), ctypes.c_int64(-1)
             _native.check(lib.cw_wait(self._h, ticket, ctypes.byref(ready), ctypes.byref(fidx)), self._h)
-            return self._wrap(int(fidx.value), res, pred, vidx) if ready.value else None
+            return self._wrap(int(fidx.value), res, pred, vidx, ticket=ticket) if ready.value else None
 
         for frame in frames:
             frame = np.ascontiguousarray(frame, dtype=np.float32)
@@ -340,13 +355,34 @@ class Pipeline:
         for dst, src in ((res, res_p), (pred, pred_p), (vidx, vidx_p)):
             _native.check(lib.cw_copy_to_host(self._h, dst.ctypes.data, src, dst.nbytes), self._h)
         self.last_timings = {"pipeline": time.perf_counter() - t0}
-        return self._wrap(int(fidx.value), res, pred, vidx)
+        return self._wrap(int(fidx.value), res, pred, vidx, ticket=self.frames_seen - 1)
 
-    def _wrap(self, frame_index, res, pred, vidx) -> WhitenedOutput:
+    def _wrap(self, frame_index, res, pred, vidx, ticket=None) -> WhitenedOutput:
         codes = vidx.view(np.uint16).reshape(vidx.shape[:2])
-        return WhitenedOutput(frame_index=frame_index, residual=res, prediction=pred,
-                              velocity=_LazyVelocityField(codes, self._lut_i, self._lut_v),
-                              mask=self.mask, imag_peak=0.0)
+        out = WhitenedOutput(frame_index=frame_index, residual=res, prediction=pred,
+                             velocity=_LazyVelocityField(codes, self._lut_i, self._lut_v),
+                             mask=self.mask, imag_peak=0.0)
+        if self._detect and ticket is not None:
+            out.detections, out.metrics = self._fetch_detections(ticket)
+        return out
+
+    def _fetch_detections(self, ticket):
+        lib = _native.load()
+        n = ctypes.c_int32(0)
+        buf = np.empty((self._max_det, 3), np.float32)
+        st = np.zeros(5, np.float64)
+        _native.check(lib.cw_detections(self._h, int(ticket), ctypes.byref(n), _native.fptr(buf), self._max_det,
+                                        st.ctypes.data_as(ctypes.POINTER(ctypes.c_double))), self._h)
+        k = min(n.value, self._max_det)
+        det = buf[:k].astype(np.float64)
+        det = det[np.lexsort((det[:, 0], det[:, 1]))] if k else det
+        nval = int(st[4])
+        metrics = {
+            "peak_abs_residual": float(st[0]), "peak_x": int(st[1]), "peak_y": int(st[2]),
+            "residual_rms": float(np.sqrt(st[3] / nval)) if nval else 0.0,
+            "n_valid": nval, "n_detections": int(n.value), "truncated": n.value > self._max_det,
+        }
+        return det, metrics
 
     # -- parity views (tests) ------------------------------------------------
 

@@ -277,3 +277,34 @@ def test_lazy_velocity_field_contract(params):
     lag = np.asarray(params.lag_grid_x)
     assert np.array_equal(v.velocities[..., 0], lag[v.indices[..., 0]])
     assert np.array_equal(v.velocities[..., 1], lag[v.indices[..., 1]])
+
+
+@pytest.mark.parametrize("stream", [False, True])
+def test_detection_epilogue_matches_host_metrics(params, stream):
+    """Fused final threshold + metrics (cli.compute_metrics_row without
+    truth, cli.py:157-208): peak |res| and its first row-major location over
+    the valid mask, RMS over the mask, and every |res| >= tau."""
+    from paper_1408_3526_b200 import Pipeline
+    from paper_1408_3526_b200.scenegen import SimConfig, generate
+
+    frames, _ = generate(SimConfig(width=96, height=80, frame_count=14, rng_seed=3))
+    tau = 0.3
+    with Pipeline(params, 96, 80, detect_threshold=tau, max_detections=4096) as pipe:
+        outs = list(pipe.process_stream(frames)) if stream else \
+            [o for o in (pipe.process_frame(f) for f in frames) if o is not None]
+    assert len(outs) == 10
+    for o in outs:
+        m = o.metrics
+        absres = np.abs(o.residual.astype(np.float64))
+        masked = np.where(o.mask, absres, -1.0)
+        py, px = np.unravel_index(int(np.argmax(masked)), absres.shape)
+        assert (m["peak_x"], m["peak_y"]) == (px, py)
+        assert m["peak_abs_residual"] == pytest.approx(absres[py, px], rel=1e-6)
+        assert m["n_valid"] == int(o.mask.sum())
+        rms = np.sqrt(np.mean(o.residual[o.mask].astype(np.float64) ** 2))
+        assert m["residual_rms"] == pytest.approx(rms, rel=1e-5)
+        ys, xs = np.nonzero(o.mask & (np.abs(o.residual) >= np.float32(tau)))
+        assert m["n_detections"] == len(xs) and not m["truncated"]
+        assert np.array_equal(o.detections[:, 0].astype(int), xs)
+        assert np.array_equal(o.detections[:, 1].astype(int), ys)
+        assert np.array_equal(o.detections[:, 2].astype(np.float32), o.residual[ys, xs])
