@@ -133,14 +133,15 @@ int cw_push_inplace(cw_handle *h, int32_t *ready, int64_t *frame_index, void *st
 
 int64_t cw_frames_seen(const cw_handle *h);
 
-/* Enable/disable the parity dump of the spectrum S (observer output). */
+/* Kept for ABI stability: the spectrum view (cw_read_view 0) is rebuilt
+ * from the observer state, S = conj(w(kz)) z / sqrt(Mx My Mz); no flag needed. */
 int cw_set_debug(cw_handle *h, int32_t on);
 
 /*
  * Parity views (tests only), copied to host after synchronising:
  *  what = 0: spectrum S of the last frame, (H, W, Mz, My, Mx) complex128
- *            (reference SpectrumField.bins layout, spectrum.py:107-135;
- *            requires cw_set_debug(h, 1) before the push)
+ *            (reference SpectrumField.bins layout, spectrum.py:107-135),
+ *            rebuilt from the stored observer state
  *  what = 1: smoothed kz-collapsed state T^ (H, W, My, Mx) complex128
  *            (R^ = autocorr of T^, flow.py:87-114)
  *  what = 2: raw observer state, float32, kernel layout

@@ -528,12 +528,7 @@ int cw_set_debug(cw_handle *h, int32_t on)
 {
     if (!h)
         return CW_ERR_VALUE;
-    h->debug = on != 0;
-    if (h->debug && !h->d_dbg) {
-        CW_CUDA(h, cudaSetDevice(h->device));
-        CW_CUDA(h, cudaMalloc(&h->d_dbg, h->state_floats * 4));
-        CW_CUDA(h, cudaMemset(h->d_dbg, 0, h->state_floats * 4));
-    }
+    h->debug = on != 0;  // the spectrum view is rebuilt from the observer state
     return CW_OK;
 }
 
@@ -569,7 +564,6 @@ static int run_frame(cw_handle *h, cudaStream_t s, int32_t *ready, int64_t *fram
     a.res = h->d_res + set * HW;
     a.pred = h->d_pred + set * HW;
     a.vidx = h->d_vidx + set * HW * 2;
-    a.dbgS = h->debug ? reinterpret_cast<float2 *>(h->d_dbg) : nullptr;
     a.W = h->W;
     a.H = h->H;
     a.NXB = h->NXB;
@@ -889,17 +883,19 @@ int cw_read_view(cw_handle *h, int32_t what, void *dst, size_t bytes)
         const size_t nb = (size_t)Mx * My * Mz;
         if (bytes != (size_t)H * W * nb * 16)
             return fail(h, CW_ERR_VALUE, "view size mismatch");
-        if (!h->d_dbg)
-            return fail(h, CW_ERR_VALUE, "spectrum view needs cw_set_debug(h, 1) before the push");
+        // the stored state is z = w(kz) z+ of the last frame: S = norm conj(w) z
         std::vector<float> pk(h->state_floats);
-        CW_CUDA(h, cudaMemcpy(pk.data(), h->d_dbg, h->state_floats * 4, cudaMemcpyDeviceToHost));
+        CW_CUDA(h, cudaMemcpy(pk.data(), h->d_state, h->state_floats * 4, cudaMemcpyDeviceToHost));
+        const double PI = 3.14159265358979323846, norm = 1.0 / std::sqrt((double)Mx * My * Mz);
         double *o = static_cast<double *>(dst);
         const int NSP = h->fn.nsp;
         const int row0 = (KZ + 1) + KX * Mz, rown = Mx * Mz;
         for (int y = 0; y < H; y++)
             for (int x = 0; x < W; x++) {
                 const size_t pb = ((size_t)y * W + x) * nb;
-                auto put = [&](int kz, int ky, int kx, double re, double im) {
+                auto put = [&](int kz, int ky, int kx, double zr, double zi) {
+                    const double c = std::cos(2 * PI * kz / Mz), sn = -std::sin(2 * PI * kz / Mz);
+                    const double re = norm * (c * zr - sn * zi), im = norm * (c * zi + sn * zr);
                     size_t i = pb + (((size_t)(kz + KZ) * My + (ky + KY)) * Mx + (kx + KX));
                     o[2 * i] = re;
                     o[2 * i + 1] = im;

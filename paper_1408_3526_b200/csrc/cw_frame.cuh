@@ -24,9 +24,10 @@
 // the observer state is float2 P[pair][lane] (re/im pairs, lane-minor), so
 // one (row, block) is a single contiguous 52 KB span.  Each row's packet is
 // brought into shared memory by TMA bulk copies (cp.async.bulk + mbarrier)
-// issued a phase ahead; the observer writes the updated state straight back
-// to HBM with 256-byte coalesced stores and overwrites the staged copy in
-// place with the Hann-conditioned spectrum that the neighbouring rows need.
+// issued as soon as the previous row has released the buffer; the observer
+// writes the updated state straight back to HBM with 256-byte coalesced
+// stores and overwrites the staged copy in place with the Hann-conditioned
+// spectrum that the neighbouring rows need.  Per row: 4 CTA barriers.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -73,7 +74,6 @@ struct FrameArgs {
     float *res;            // (H, W) residual out
     float *pred;           // (H, W) prediction out (nullable)
     uint8_t *vidx;         // (H, W, 2) velocity index out
-    float2 *dbgS;          // spectrum dump, state-packet layout (nullable)
     int W, H, NXB;
     int y_begin;           // first local anchor row (strip halo)
     int y_off;             // global row of local row 0
@@ -144,9 +144,8 @@ struct Geo {
     __host__ __device__ static constexpr int spair(int r) { return r == 0 ? 0 : ROW0P + (r - 1) * ROWNP; }
     __host__ __device__ static constexpr int tpair(int r) { return r == 0 ? 0 : TROW0P + (r - 1) * TROWNP; }
     __host__ __device__ static constexpr int ppair(int r) { return r == 0 ? 0 : PROW0P + (r - 1) * PROWNP; }
-    // shared memory plan (bytes); the stage also holds B(ky, lx) = NR x MAXL pairs
-    static constexpr int STAGEP = NSP > NR * MAXL ? NSP : NR * MAXL;
-    static constexpr int SM_STAGE = STAGEP * 32 * 8;  // state packet -> Cx in place -> B(ky,lx)
+    // shared memory plan (bytes)
+    static constexpr int SM_STAGE = NSP * 32 * 8;     // state packet -> Cx in place
     static constexpr int SM_TSTAGE = NTP * 32 * 8;    // T^ packet
     static constexpr int SM_RET = RETP * 32 * 8;      // retained z+
     static constexpr int SM_XF = RING * XF * 32 * 4;  // x-stage ring
@@ -232,7 +231,6 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
     float *ppef = reinterpret_cast<float *>(reinterpret_cast<unsigned char *>(pbest) + G::SM_BEST);
     uint16_t *srank = reinterpret_cast<uint16_t *>(reinterpret_cast<unsigned char *>(ppef) + G::SM_PEF);
     uint64_t *bar = reinterpret_cast<uint64_t *>(reinterpret_cast<unsigned char *>(srank) + G::SM_RANK);
-    float2 *bb = stage;  // B(ky, lx) after the Hy reads: [NR][MAXL][32]
 
     const int lane = threadIdx.x & 31;
     const int r = threadIdx.x >> 5;  // spatial-frequency row ky of this warp
@@ -245,26 +243,37 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
     const bool use_that = a.ready && !a.first;
 
     for (int i = threadIdx.x; i < nlx * nly; i += G::NTHREADS) srank[i] = t.rank[i];
+    uint64_t *bar_t = bar + 1;  // bar: observer-state packet, bar_t: T^ packet
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
+        mbar_init(bar_t, 1);
         fence_mbar_init();
     }
     __syncthreads();
-    uint32_t phase = 0;
+    uint32_t phase = 0, phase_t = 0;
 
-    // one elected thread stages the (row, block) packets of the next row
+    // one elected thread stages the (row, block) packets of the next row;
+    // the state and T^ packets are freed at different barriers
+    constexpr int ISSUER = G::NTHREADS - 32;  // lane 0 of warp KY: no PEF work, fewest lag columns
     auto issue = [&](int yy, int xb) {
-        if (threadIdx.x == 0) {
+        if (threadIdx.x == ISSUER) {
             const size_t pix = (size_t)yy * NXB + xb;
             fence_proxy_async();  // prior generic smem accesses before the async-proxy writes
-            const uint32_t bs = G::NSP * 32 * 8, bt = use_that ? G::SM_TSTAGE : 0;
-            mbar_expect_tx(bar, bs + bt);
+            constexpr uint32_t bs = G::NSP * 32 * 8;
+            mbar_expect_tx(bar, bs);
             const unsigned char *src = reinterpret_cast<const unsigned char *>(a.state + pix * G::NSP * 32);
-            constexpr uint32_t CH = (G::NSP * 32 * 8 / 4 + 15) / 16 * 16;
+            constexpr uint32_t CH = (bs / 4 + 15) / 16 * 16;
             for (uint32_t off = 0; off < bs; off += CH)
                 tma_load(reinterpret_cast<unsigned char *>(stage) + off, src + off, (bs - off) < CH ? (bs - off) : CH,
                          bar);
-            if (bt) tma_load(tstage, a.that + pix * G::NTP * 32, bt, bar);
+        }
+    };
+    auto issue_t = [&](int yy, int xb) {
+        if (use_that && threadIdx.x == ISSUER) {
+            const size_t pix = (size_t)yy * NXB + xb;
+            fence_proxy_async();
+            mbar_expect_tx(bar_t, G::SM_TSTAGE);
+            tma_load(tstage, a.that + pix * G::NTP * 32, G::SM_TSTAGE, bar_t);
         }
     };
 
@@ -324,6 +333,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
         fence_proxy_async();
         __syncthreads();  // previous chunk done with the stage and the ring
         issue(ys, xb);
+        issue_t(ys, xb);
         for (int k = r; k < MY; k += NR) {
             const int yy = ys - MY + 1 + k;
             xstage(yy, x, ring_slot(yy));
@@ -357,7 +367,6 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
             const bool anchor = colv && x >= MX - 1 && (yy + a.y_off) >= MY - 1;
             const size_t pix = (size_t)yy * NXB + xb;
             float2 *stg = a.state + (pix * G::NSP + G::spair(r)) * 32 + lane;
-            float2 *dbg = a.dbgS ? a.dbgS + (pix * G::NSP + G::spair(r)) * 32 + lane : nullptr;
             float2 *sst = stage + G::spair(r) * 32 + lane;
             mbar_wait(bar, phase);
             phase ^= 1;
@@ -380,13 +389,11 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                     const float z0 = zd[0].r + e;
                     stg[0] = make_float2(z0, 0.f);
                     sret[lane] = make_float2(z0, 0.f);
-                    if (dbg) dbg[0] = make_float2(t.norm * z0, 0.f);
 #pragma unroll
                     for (int kz = 1; kz <= KZ; kz++) {
                         const cf zp = cmk(zd[kz].r + e, zd[kz].i);
                         stg[kz * 32] = f2(cmul(cmk(t.wc[kz + KZ], t.ws[kz + KZ]), zp));
                         sret[kz * 32 + lane] = f2(zp);
-                        if (dbg) dbg[kz * 32] = make_float2(t.norm * zp.r, t.norm * zp.i);
                     }
                 }
                 // DC suppression (_kernels.py:167-174): C(kz, 0, 0) = 0
@@ -411,7 +418,6 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                         const cf zn = (kzi == KZ) ? zp[kzi] : cmul(cmk(t.wc[kzi], t.ws[kzi]), zp[kzi]);
                         stg[(base + kzi) * 32] = f2(zn);
                         if (kx <= BX) sret[(base + kzi) * 32 + lane] = f2(zp[kzi]);
-                        if (dbg) dbg[(base + kzi) * 32] = make_float2(t.norm * zp[kzi].r, t.norm * zp[kzi].i);
                     }
 #pragma unroll
                     for (int kzi = 0; kzi < MZ; kzi++)
@@ -459,7 +465,6 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                         const cf zn = (kzi == KZ) ? zp[kzi] : cmul(cmk(t.wc[kzi], t.ws[kzi]), zp[kzi]);
                         stg[(kxi * MZ + kzi) * 32] = f2(zn);
                         if (r <= BY && kxb >= 0 && kxb < G::WX) rr[(kxb * MZ + kzi) * 32] = f2(zp[kzi]);
-                        if (dbg) dbg[(kxi * MZ + kzi) * 32] = make_float2(t.norm * zp[kzi].r, t.norm * zp[kzi].i);
                     }
 #pragma unroll
                     for (int kzi = 0; kzi < MZ; kzi++)
@@ -484,10 +489,12 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
             }
 
             // ---------------- phase C1: Hy, power, kz collapse, smoothing ----------------
-            cf T[MX];
+            // T^ of this warp's row -> HBM and, in place, to the T^ stage where
+            // every warp reads all rows for the lag contraction
             {
                 float2 *thg = a.that + (pix * G::NTP + G::tpair(r)) * 32 + lane;
-                const float2 *tho = tstage + G::tpair(r) * 32 + lane;
+                float2 *tho = tstage + G::tpair(r) * 32 + lane;
+                cf T[MX];
                 if (r == 0) {
 #pragma unroll
                     for (int kx = 0; kx <= KX; kx++) {
@@ -502,21 +509,6 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                             acc.i = fmaf(t.azs[kz + KZ], p, acc.i);
                         }
                         T[KX + kx] = acc;
-                    }
-                    // smoothing of T^ (_kernels.py:261-271; first ready frame copies)
-                    float v = T[KX].r;
-                    if (!a.first) v = fmaf(t.beta, v, t.alpha * tho[0].x);
-                    thg[0] = make_float2(v, 0.f);
-                    T[KX] = cmk(v, 0.f);
-#pragma unroll
-                    for (int kx = 1; kx <= KX; kx++) {
-                        cf v2 = T[KX + kx];
-                        if (!a.first) {
-                            const float2 o = tho[kx * 32];
-                            v2 = cmk(fmaf(t.beta, v2.r, t.alpha * o.x), fmaf(t.beta, v2.i, t.alpha * o.y));
-                        }
-                        thg[kx * 32] = f2(v2);
-                        T[KX + kx] = v2;
                     }
                 } else {
 #pragma unroll
@@ -533,105 +525,49 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                             acc.r = fmaf(t.azc[kzi], p, acc.r);
                             acc.i = fmaf(t.azs[kzi], p, acc.i);
                         }
-                        cf v2 = acc;
-                        if (!a.first) {
-                            const float2 o = tho[kxi * 32];
-                            v2 = cmk(fmaf(t.beta, v2.r, t.alpha * o.x), fmaf(t.beta, v2.i, t.alpha * o.y));
-                        }
-                        thg[kxi * 32] = f2(v2);
-                        T[kxi] = v2;
+                        T[kxi] = acc;
                     }
+                }
+                // smoothing of T^ (_kernels.py:261-271; first ready frame copies)
+                if (use_that) {
+                    mbar_wait(bar_t, phase_t);
+                    phase_t ^= 1;
+                }
+                const int k0 = (r == 0) ? KX : 0;
+#pragma unroll
+                for (int kxi = 0; kxi < MX; kxi++) {
+                    if (kxi < k0) continue;
+                    const int j = (r == 0) ? kxi - KX : kxi;  // pair index within the row
+                    cf v2 = T[kxi];
+                    if (r == 0 && kxi == KX) v2.i = 0.f;  // T(0,0) is real
+                    if (!a.first) {
+                        const float2 o = tho[j * 32];
+                        v2 = cmk(fmaf(t.beta, v2.r, t.alpha * o.x), fmaf(t.beta, v2.i, t.alpha * o.y));
+                    }
+                    thg[j * 32] = f2(v2);
+                    tho[j * 32] = f2(v2);
                 }
             }
-            __syncthreads();  // (2) Hy reads of the stage done: it now holds B(ky, lx)
+            fence_proxy_async();  // Hy reads of the stage before the next TMA write
+            __syncthreads();  // (2) T^ rows visible; the state stage is free
+            if (yy + 1 < ye) issue(yy + 1, xb);
 
-            // ---------------- phase C2: stage-1 lag contraction along kx ----------------
-            // B(ky, lx) = gx(lx) sum_kx e^{-j 2 pi kx lx / Mx} T^(ky, kx)
-#define BB(rr, lx) bb[((rr) * MAXL + (lx)) * 32 + lane]
-            if (NL && t.sym_x) {
-                constexpr int C0 = NL / 2;  // lag 0; lags +-q at C0 +- q
-                if (r == 0) {
-#pragma unroll
-                    for (int q = 0; q <= C0; q++) {
-                        float cp = t.s1g[C0 + q] * T[KX].r, sp2 = 0.f;
-#pragma unroll
-                        for (int kx = 1; kx <= KX; kx++) {
-                            cp = fmaf(2.f * t.s1c[C0 + q][kx - 1], T[KX + kx].r, cp);
-                            sp2 = fmaf(2.f * t.s1s[C0 + q][kx - 1], T[KX + kx].i, sp2);
-                        }
-                        BB(0, C0 + q) = make_float2(cp + sp2, 0.f);
-                        BB(0, C0 - q) = make_float2(cp - sp2, 0.f);
-                    }
-                } else {
-                    cf A[KX + 1], D[KX + 1];
-#pragma unroll
-                    for (int kx = 1; kx <= KX; kx++) {
-                        A[kx] = cadd(T[KX + kx], T[KX - kx]);
-                        D[kx] = csub(T[KX + kx], T[KX - kx]);
-                    }
-#pragma unroll
-                    for (int q = 0; q <= C0; q++) {
-                        const float g = t.s1g[C0 + q];
-                        float cr = g * T[KX].r, ci = g * T[KX].i, sr = 0.f, si = 0.f;
-#pragma unroll
-                        for (int kx = 1; kx <= KX; kx++) {
-                            const float c = t.s1c[C0 + q][kx - 1], s = t.s1s[C0 + q][kx - 1];
-                            cr = fmaf(c, A[kx].r, cr);
-                            ci = fmaf(c, A[kx].i, ci);
-                            sr = fmaf(s, D[kx].i, sr);
-                            si = fmaf(-s, D[kx].r, si);
-                        }
-                        BB(r, C0 + q) = make_float2(cr + sr, ci + si);
-                        BB(r, C0 - q) = make_float2(cr - sr, ci - si);
-                    }
-                }
-            } else {
-                if (r == 0) {
-                    for (int lx = 0; lx < nlx; lx++) {
-                        float b = t.s1g[lx] * T[KX].r;
-#pragma unroll
-                        for (int kx = 1; kx <= KX; kx++) {
-                            b = fmaf(2.f * t.s1c[lx][kx - 1], T[KX + kx].r, b);
-                            b = fmaf(2.f * t.s1s[lx][kx - 1], T[KX + kx].i, b);
-                        }
-                        BB(0, lx) = make_float2(b, 0.f);
-                    }
-                } else {
-                    cf A[KX + 1], D[KX + 1];
-#pragma unroll
-                    for (int kx = 1; kx <= KX; kx++) {
-                        A[kx] = cadd(T[KX + kx], T[KX - kx]);
-                        D[kx] = csub(T[KX + kx], T[KX - kx]);
-                    }
-                    for (int lx = 0; lx < nlx; lx++) {
-                        const float g = t.s1g[lx];
-                        float br = g * T[KX].r, bi = g * T[KX].i;
-#pragma unroll
-                        for (int kx = 1; kx <= KX; kx++) {
-                            const float c = t.s1c[lx][kx - 1], s = t.s1s[lx][kx - 1];
-                            br = fmaf(c, A[kx].r, fmaf(s, D[kx].i, br));
-                            bi = fmaf(c, A[kx].i, fmaf(-s, D[kx].r, bi));
-                        }
-                        BB(r, lx) = make_float2(br, bi);
-                    }
-                }
-            }
-            __syncthreads();  // (3) B(ky, lx) visible
-
-            // ---------------- phase D: stage-2 contraction along ky + partial argmax ----------------
-            // score(ly, lx) = gy gx R^(ly, lx) = s2g B0 + sum_ky s2c Re B + s2s Im B
+            // ---------------- phase CD: lag contraction + partial argmax ----------------
+            // score(ly, lx) = gy gx R^(ly, lx); stage 1 along kx (B(ky, lx)) for
+            // this warp's lag columns, straight into stage 2 along ky and the pick.
             {
                 float best = -INFINITY;
                 int brk = 0x7fffffff;
-                for (int lx = r; lx < nlx; lx += NR) {
-                    const float b0 = BB(0, lx).x;
-                    float br[KY + 1], bi[KY + 1];
-#pragma unroll
-                    for (int k = 1; k <= KY; k++) {
-                        const float2 v = BB(k, lx);
-                        br[k] = v.x;
-                        bi[k] = v.y;
+                // T^(ky, kx) of the staged rows (row 0: kx >= 0, (0,0) real)
+                auto tv = [&](int ky, int kx) -> cf {
+                    if (ky == 0) {
+                        const cf v = c2(tstage[(kx >= 0 ? kx : -kx) * 32 + lane]);
+                        return kx >= 0 ? v : cconj(v);
                     }
+                    return c2(tstage[(G::tpair(ky) + kx + KX) * 32 + lane]);
+                };
+                // stage 2 + in-column argmax for one column whose B values are given
+                auto column = [&](int lx, float b0, const float *br, const float *bi) {
                     if (NL && t.sym_y) {
                         // visit ly = 0, -1, +1, -2, +2, ...: ascending rank order within
                         // a column (|v|^2 grows with |ly|, then iy ascending); two
@@ -675,13 +611,89 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                             if (better(v, rk, best, brk)) { best = v; brk = rk; }
                         }
                     }
+                };
+                if (NL && t.sym_x) {
+                    // +-lx pairing: this warp owns |lx| = C0 + q for q = r, r + NR, ...
+                    constexpr int C0 = NL / 2;
+                    for (int q = r; q <= C0; q += NR) {
+                        const int lp = C0 + q;
+                        const float g = t.s1g[lp];
+                        float c1[KX + 1], s1[KX + 1];
+#pragma unroll
+                        for (int kx = 1; kx <= KX; kx++) {
+                            c1[kx] = t.s1c[lp][kx - 1];
+                            s1[kx] = t.s1s[lp][kx - 1];
+                        }
+                        float bp0, bm0, brp[KY + 1], bip[KY + 1], brm[KY + 1], bim[KY + 1];
+                        {   // row 0: T(0,-kx) = conj T(0,kx)
+                            float cp = g * tv(0, 0).r, sp2 = 0.f;
+#pragma unroll
+                            for (int kx = 1; kx <= KX; kx++) {
+                                const cf v = tv(0, kx);
+                                cp = fmaf(2.f * c1[kx], v.r, cp);
+                                sp2 = fmaf(2.f * s1[kx], v.i, sp2);
+                            }
+                            bp0 = cp + sp2;
+                            bm0 = cp - sp2;
+                        }
+#pragma unroll
+                        for (int ky = 1; ky <= KY; ky++) {
+                            const cf t0 = tv(ky, 0);
+                            float cr = g * t0.r, ci = g * t0.i, sr = 0.f, si = 0.f;
+#pragma unroll
+                            for (int kx = 1; kx <= KX; kx++) {
+                                const cf tp = tv(ky, kx), tm = tv(ky, -kx);
+                                const cf A = cadd(tp, tm), D = csub(tp, tm);
+                                cr = fmaf(c1[kx], A.r, cr);
+                                ci = fmaf(c1[kx], A.i, ci);
+                                sr = fmaf(s1[kx], D.i, sr);
+                                si = fmaf(-s1[kx], D.r, si);
+                            }
+                            brp[ky] = cr + sr;
+                            bip[ky] = ci + si;
+                            brm[ky] = cr - sr;
+                            bim[ky] = ci - si;
+                        }
+                        column(C0 + q, bp0, brp, bip);
+                        if (q) column(C0 - q, bm0, brm, bim);
+                    }
+                } else {
+                    for (int lx = r; lx < nlx; lx += NR) {
+                        const float g = t.s1g[lx];
+                        float b0, br[KY + 1], bi[KY + 1];
+                        {
+                            float b = g * tv(0, 0).r;
+#pragma unroll
+                            for (int kx = 1; kx <= KX; kx++) {
+                                const cf v = tv(0, kx);
+                                b = fmaf(2.f * t.s1c[lx][kx - 1], v.r, b);
+                                b = fmaf(2.f * t.s1s[lx][kx - 1], v.i, b);
+                            }
+                            b0 = b;
+                        }
+#pragma unroll
+                        for (int ky = 1; ky <= KY; ky++) {
+                            const cf t0 = tv(ky, 0);
+                            float xr = g * t0.r, xi = g * t0.i;
+#pragma unroll
+                            for (int kx = 1; kx <= KX; kx++) {
+                                const cf tp = tv(ky, kx), tm = tv(ky, -kx);
+                                const cf A = cadd(tp, tm), D = csub(tp, tm);
+                                const float c = t.s1c[lx][kx - 1], s = t.s1s[lx][kx - 1];
+                                xr = fmaf(c, A.r, fmaf(s, D.i, xr));
+                                xi = fmaf(c, A.i, fmaf(-s, D.r, xi));
+                            }
+                            br[ky] = xr;
+                            bi[ky] = xi;
+                        }
+                        column(lx, b0, br, bi);
+                    }
                 }
                 pbest[r * 32 + lane] = make_float2(best, __int_as_float(brk));
             }
-#undef BB
-            fence_proxy_async();  // stage reads before the next TMA write
-            __syncthreads();  // (4) partial maxima visible; the stage is free
-            if (yy + 1 < ye) issue(yy + 1, xb);
+            fence_proxy_async();  // T^ stage reads before the next TMA write
+            __syncthreads();  // (3) partial maxima visible; the T^ stage is free
+            if (yy + 1 < ye) issue_t(yy + 1, xb);
 
             // ---------------- phase E: final pick, PEF partial per row ----------------
             int vix, viy;
@@ -728,7 +740,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                 uint8_t *vp = a.vidx + ((size_t)yy * W + x) * 2;
                 *reinterpret_cast<uchar2 *>(vp) = make_uchar2((uint8_t)vix, (uint8_t)viy);
             }
-            __syncthreads();  // (5) PEF partials visible
+            __syncthreads();  // (4) PEF partials visible
 
             // ---------------- phase F: residual (+ threshold epilogue) ----------------
             if (r == 0) {
