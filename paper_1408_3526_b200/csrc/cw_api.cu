@@ -808,6 +808,17 @@ int cw_detections(cw_handle *h, int64_t ticket, int32_t *n_total, float *xyr, in
     return CW_OK;
 }
 
+#ifdef CW_PHASE_TIMING
+extern "C" int cw_phase_clocks(unsigned long long *dst)  // [8][16], then zeroed
+{
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(dst, cw_phase_clk, sizeof(unsigned long long) * 128);
+    static unsigned long long zero[128] = {};
+    cudaMemcpyToSymbol(cw_phase_clk, zero, sizeof zero);
+    return 0;
+}
+#endif
+
 int cw_copy_to_host(cw_handle *h, void *dst, const void *src_dev, size_t bytes)
 {
     if (!h || !dst || !src_dev)

@@ -38,6 +38,9 @@ constexpr int MAXK = 5;    // largest half window supported by the tables
 constexpr int MAXM = 2 * MAXK + 1;
 constexpr int MAXL = 33;   // largest lag grid per axis
 constexpr int RESTART = 32;  // rows between direct y-SDFT restarts (bounds f32 drift)
+#ifndef CW_FENCE_ALL
+#define CW_FENCE_ALL 1  // every thread orders its generic stage reads before the next TMA write
+#endif
 
 struct Tables {
     // x stage: cos/sin(2 pi kx m / Mx), kx = 0..KX, m = 0..Mx-1
@@ -152,9 +155,11 @@ struct Geo {
     static constexpr int SM_BEST = NR * 32 * 8;       // partial argmax (score, rank)
     static constexpr int SM_PEF = (BY + 1) * 32 * 4;
     static constexpr int SM_RANK = ((MAXL * MAXL * 2) + 15) / 16 * 16;
+    static constexpr int SM_ROW = ((32 + MX - 1) * 4 + 15) / 16 * 16;  // next frame row segment
+    static constexpr int SM_DEL = 32 * 4;                               // delayed-frame values
     static constexpr int SM_BAR = 16;
     static constexpr size_t SMEM_BYTES =
-        SM_STAGE + SM_TSTAGE + SM_RET + SM_XF + SM_BEST + SM_PEF + SM_RANK + SM_BAR;
+        SM_STAGE + SM_TSTAGE + SM_RET + SM_XF + SM_BEST + SM_PEF + SM_RANK + SM_ROW + SM_DEL + SM_BAR;
 };
 
 struct cf {
@@ -214,10 +219,37 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase)
     } while (!ok);
 }
 
+#ifdef CW_PHASE_TIMING
+// per-warp clock64 accumulators (phase-timing builds only): [warp][event]
+__device__ unsigned long long cw_phase_clk[8][16];
+#define CW_STAMP(k)                                                                       \
+    do {                                                                                  \
+        const unsigned long long now = clock64();                                         \
+        clk_acc[k] += now - clk_prev;                                                     \
+        clk_prev = now;                                                                   \
+    } while (0)
+#else
+#define CW_STAMP(k) \
+    do {            \
+    } while (0)
+#endif
+
+// 4-byte cp.async (LDGSTS) with zero fill when !valid (src-size 0)
+__device__ __forceinline__ void cp_async4(void *dst, const float *src, bool valid)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_addr(dst)), "l"(src), "r"(valid ? 4 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 template <class G, int NL>
 __global__ void __launch_bounds__(G::NTHREADS, 2)
 cw_frame_kernel(const FrameArgs a, const Tables t)
 {
+#ifdef CW_PHASE_TIMING
+    unsigned long long clk_prev = clock64();
+    unsigned long long clk_acc[11] = {};
+#endif
     constexpr int KX = G::KX, KY = G::KY, KZ = G::KZ, BX = G::BX, BY = G::BY;
     constexpr int MX = G::MX, MY = G::MY, MZ = G::MZ;
     constexpr int NR = G::NR, RING = G::RING;
@@ -230,7 +262,9 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
     float2 *pbest = reinterpret_cast<float2 *>(smem_raw + G::SM_STAGE + G::SM_TSTAGE + G::SM_RET + G::SM_XF);
     float *ppef = reinterpret_cast<float *>(reinterpret_cast<unsigned char *>(pbest) + G::SM_BEST);
     uint16_t *srank = reinterpret_cast<uint16_t *>(reinterpret_cast<unsigned char *>(ppef) + G::SM_PEF);
-    uint64_t *bar = reinterpret_cast<uint64_t *>(reinterpret_cast<unsigned char *>(srank) + G::SM_RANK);
+    float *rowbuf = reinterpret_cast<float *>(reinterpret_cast<unsigned char *>(srank) + G::SM_RANK);
+    float *delbuf = reinterpret_cast<float *>(reinterpret_cast<unsigned char *>(rowbuf) + G::SM_ROW);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(reinterpret_cast<unsigned char *>(delbuf) + G::SM_DEL);
 
     const int lane = threadIdx.x & 31;
     const int r = threadIdx.x >> 5;  // spatial-frequency row ky of this warp
@@ -302,6 +336,34 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
 #pragma unroll
         for (int f = 0; f < G::XF; f++) XFR(slot, f) = acc[f];
     };
+    // same sums from the row segment prefetched into rowbuf (cp.async):
+    // rowbuf[i] = frame[row][x0 - (MX-1) + i], zero outside the frame
+    auto xstage_s = [&](int slot) {
+        float acc[G::XF];
+#pragma unroll
+        for (int f = 0; f < G::XF; f++) acc[f] = 0.f;
+#pragma unroll
+        for (int m = 0; m < MX; m++) {
+            const float v = rowbuf[lane + MX - 1 - m];
+            acc[0] += v;
+#pragma unroll
+            for (int k = 1; k <= KX; k++) {
+                acc[2 * k - 1] = fmaf(t.exc[k][m], v, acc[2 * k - 1]);
+                acc[2 * k] = fmaf(t.exs[k][m], v, acc[2 * k]);
+            }
+        }
+#pragma unroll
+        for (int f = 0; f < G::XF; f++) XFR(slot, f) = acc[f];
+    };
+    auto prefetch_row = [&](int yy, int x0) {  // async: the next row's 32 + MX - 1 samples
+        const bool rv = yy >= 0 && yy < H;
+        const float *row = a.frame + (size_t)(rv ? yy : 0) * W;
+        for (int i = lane; i < 32 + MX - 1; i += 32) {
+            const int gx = x0 - (MX - 1) + i;
+            const bool v = rv && gx >= 0 && gx < W;
+            cp_async4(rowbuf + i, v ? row + gx : a.frame, v);
+        }
+    };
     auto ring_slot = [&](int yy) { return ((yy % RING) + RING) % RING; };
     auto xfv = [&](int slot, int kx) -> cf {
         if (kx == 0) return cmk(XFR(slot, 0), 0.f);
@@ -330,7 +392,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
         const int x = xb * 32 + lane;
         const bool colv = x < W;
 
-        fence_proxy_async();
+        if (CW_FENCE_ALL) fence_proxy_async();
         __syncthreads();  // previous chunk done with the stage and the ring
         issue(ys, xb);
         issue_t(ys, xb);
@@ -346,7 +408,8 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
 
         for (int yy = ys; yy < ye; yy++) {
             // ---------------- phase B: spatial SDFT, observer, Hz, Hx ----------------
-            if (r == 0 && yy + 1 < ye) xstage(yy + 1, x, ring_slot(yy + 1));
+            CW_STAMP(0);  // previous row's tail (phase F / loop) -> here
+            if (!a.ready && r == KY && yy + 1 < ye) xstage(yy + 1, x, ring_slot(yy + 1));
             if (((yy - ys) % RESTART) == 0) {
                 // direct restart sum_my e^{+j 2 pi ky my / My} xf(yy - my) (_kernels.py:58-61)
 #pragma unroll
@@ -368,7 +431,9 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
             const size_t pix = (size_t)yy * NXB + xb;
             float2 *stg = a.state + (pix * G::NSP + G::spair(r)) * 32 + lane;
             float2 *sst = stage + G::spair(r) * 32 + lane;
+            CW_STAMP(1);  // x stage + y SDFT
             mbar_wait(bar, phase);
+            CW_STAMP(2);  // state TMA wait
             phase ^= 1;
 
             // Deadbeat observer on z = Mz * xhat (state in HBM, in place):
@@ -481,13 +546,21 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                         }
                 }
             }
-            if (!a.ready) fence_proxy_async();  // stage reads before the next TMA write
+            if (CW_FENCE_ALL && !a.ready) fence_proxy_async();  // stage reads before the next TMA write
+            CW_STAMP(3);  // observer + Hz + Hx
             __syncthreads();  // (1) Cx rows visible; x stage of yy+1 done
+            CW_STAMP(4);  // barrier 1 wait
             if (!a.ready) {
                 if (yy + 1 < ye) issue(yy + 1, xb);  // stage free: next row's state
                 continue;
             }
 
+            // async prefetches consumed in phases E (x stage of yy+1) and F (residual)
+            if (r == KY && yy + 1 < ye) prefetch_row(yy + 1, xb * 32);
+            if (r == 0) {
+                const size_t o = (size_t)(yy - a.mhy) * W + (x - a.mhx);
+                cp_async4(delbuf + lane, anchor ? a.delayed + o : a.frame, anchor);
+            }
             // ---------------- phase C1: Hy, power, kz collapse, smoothing ----------------
             // T^ of this warp's row -> HBM and, in place, to the T^ stage where
             // every warp reads all rows for the lag contraction
@@ -548,8 +621,10 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                     tho[j * 32] = f2(v2);
                 }
             }
-            fence_proxy_async();  // Hy reads of the stage before the next TMA write
+            if (CW_FENCE_ALL) fence_proxy_async();  // Hy reads of the stage before the next TMA write
+            CW_STAMP(5);  // C1
             __syncthreads();  // (2) T^ rows visible; the state stage is free
+            CW_STAMP(6);  // barrier 2 wait
             if (yy + 1 < ye) issue(yy + 1, xb);
 
             // ---------------- phase CD: lag contraction + partial argmax ----------------
@@ -691,11 +766,18 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                 }
                 pbest[r * 32 + lane] = make_float2(best, __int_as_float(brk));
             }
-            fence_proxy_async();  // T^ stage reads before the next TMA write
+            if (CW_FENCE_ALL) fence_proxy_async();  // T^ stage reads before the next TMA write
+            CW_STAMP(7);  // CD
             __syncthreads();  // (3) partial maxima visible; the T^ stage is free
+            CW_STAMP(8);  // barrier 3 wait
             if (yy + 1 < ye) issue_t(yy + 1, xb);
 
-            // ---------------- phase E: final pick, PEF partial per row ----------------
+            // ---------------- phase E: final pick, PEF partials; x stage of yy+1 ----------------
+            if (r == KY && yy + 1 < ye) {
+                cp_async_wait_all();
+                __syncwarp();
+                xstage_s(ring_slot(yy + 1));
+            }
             int vix, viy;
             {
                 const float2 bv = pbest[lane];
@@ -740,17 +822,20 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                 uint8_t *vp = a.vidx + ((size_t)yy * W + x) * 2;
                 *reinterpret_cast<uchar2 *>(vp) = make_uchar2((uint8_t)vix, (uint8_t)viy);
             }
+            CW_STAMP(9);  // E
             __syncthreads();  // (4) PEF partials visible
+            CW_STAMP(10);  // barrier 4 wait
 
             // ---------------- phase F: residual (+ threshold epilogue) ----------------
             if (r == 0) {
+                cp_async_wait_all();
                 float rv = 0.f;
                 if (anchor) {
                     float p = 0.f;
 #pragma unroll
                     for (int k = 0; k <= BY; k++) p += ppef[k * 32 + lane];
                     const size_t o = (size_t)(yy - a.mhy) * W + (x - a.mhx);
-                    rv = __ldg(a.delayed + o) - p;
+                    rv = delbuf[lane] - p;
                     a.res[o] = rv;
                     if (a.pred) a.pred[o] = p;
                 }
@@ -759,6 +844,10 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
         }
         u += ye - ys;
     }
+#ifdef CW_PHASE_TIMING
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0)
+        for (int k = 0; k < 11; k++) cw_phase_clk[threadIdx.x >> 5][k] += clk_acc[k];
+#endif
 #undef XFR
 }
 
