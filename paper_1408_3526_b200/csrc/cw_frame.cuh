@@ -77,6 +77,7 @@ struct FrameArgs {
     float *res;            // (H, W) residual out
     float *pred;           // (H, W) prediction out (nullable)
     uint8_t *vidx;         // (H, W, 2) velocity index out
+    const uint8_t *vidx_prev;  // previous frame's velocities (PEF coefficient prefetch guess)
     int W, H, NXB;
     int y_begin;           // first local anchor row (strip halo)
     int y_off;             // global row of local row 0
@@ -154,7 +155,7 @@ struct Geo {
     static constexpr int SM_XF = RING * XF * 32 * 4;  // x-stage ring
     static constexpr int SM_BEST = NR * 32 * 8;       // partial argmax (score, rank)
     static constexpr int SM_PEF = (BY + 1) * 32 * 4;
-    static constexpr int SM_RANK = ((MAXL * MAXL * 2) + 15) / 16 * 16;
+    static constexpr int SM_RANK = ((MAXL * MAXL * 4) + 15) / 16 * 16;  // rank u16 + (ix, iy) u8 pairs
     static constexpr int SM_ROW = ((32 + MX - 1) * 4 + 15) / 16 * 16;  // next frame row segment
     static constexpr int SM_DEL = 32 * 4;                               // delayed-frame values
     static constexpr int SM_BAR = 16;
@@ -276,7 +277,13 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
     const long long u1 = units * (blockIdx.x + 1) / gridDim.x;
     const bool use_that = a.ready && !a.first;
 
-    for (int i = threadIdx.x; i < nlx * nly; i += G::NTHREADS) srank[i] = t.rank[i];
+    uint8_t *srxy = reinterpret_cast<uint8_t *>(srank + MAXL * MAXL);  // rank -> (ix, iy)
+    for (int i = threadIdx.x; i < nlx * nly; i += G::NTHREADS) {
+        srank[i] = t.rank[i];
+        srxy[2 * i] = t.rix[i];
+        srxy[2 * i + 1] = t.riy[i];
+    }
+    const cf tw_r = cmk(t.twc[threadIdx.x >> 5], t.tws[threadIdx.x >> 5]);  // this warp's y resonator
     uint64_t *bar_t = bar + 1;  // bar: observer-state packet, bar_t: T^ packet
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
@@ -423,9 +430,8 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
             } else {
                 // comb + resonator (_kernels.py:62-68)
                 const int s1 = ring_slot(yy), s0 = ring_slot(yy - MY);
-                const cf tw = cmk(t.twc[r], t.tws[r]);
 #pragma unroll
-                for (int i = 0; i < MX; i++) sp[i] = cadd(cmul(tw, sp[i]), csub(xfv(s1, i - KX), xfv(s0, i - KX)));
+                for (int i = 0; i < MX; i++) sp[i] = cadd(cmul(tw_r, sp[i]), csub(xfv(s1, i - KX), xfv(s0, i - KX)));
             }
             const bool anchor = colv && x >= MX - 1 && (yy + a.y_off) >= MY - 1;
             const size_t pix = (size_t)yy * NXB + xb;
@@ -793,8 +799,8 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                     vix = a.forced_ix;
                     viy = a.forced_iy;
                 } else {
-                    vix = t.rix[brk];
-                    viy = t.riy[brk];
+                    vix = srxy[2 * brk];
+                    viy = srxy[2 * brk + 1];
                 }
             }
             if (r <= BY) {
