@@ -362,6 +362,152 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+# ---------------------------------------------------------------------------
+# other BASELINE.json configs (extra JSON lines; the driver's default is C3)
+# ---------------------------------------------------------------------------
+
+C5_SWEEP = {
+    "default (4,4,2,3,3) lag 1/4": dict(),
+    "(3,3,2,2,2) lag 1/4": dict(kx=3, ky=3, bx=2, by=2, mhat=(3, 3, 2)),
+    "(5,5,2,4,4) lag 1/4": dict(kx=5, ky=5, bx=4, by=4, mhat=(5, 5, 2)),
+    "(4,4,1,3,3) lag 1/4": dict(kz=1, mhat=(4, 4, 1)),
+    "(4,4,2,3,3) lag 1/2": dict(lag_grid_x=tuple(i / 2 for i in range(-4, 5)),
+                                lag_grid_y=tuple(i / 2 for i in range(-4, 5))),
+    "(4,4,2,3,3) lag 1/8": dict(lag_grid_x=tuple(i / 8 for i in range(-16, 17)),
+                                lag_grid_y=tuple(i / 8 for i in range(-16, 17))),
+}
+
+
+def _device_run(lib, pipe, frames, steps, warmup, stream, dist=None, before_push=None):
+    """Time `steps` device-resident pushes on `stream` (CUDA events, barrier
+    on both sides) after the temporal window and `warmup` frames; returns
+    (elapsed ms, mean kernel ms, launches, clocks summary)."""
+    import ctypes
+
+    import torch
+
+    from paper_1408_3526_b200 import _native
+
+    h = pipe._h
+    sh = ctypes.c_void_p(stream.cuda_stream)
+    ready, fidx = ctypes.c_int32(), ctypes.c_int64()
+    nf = frames.shape[0]
+
+    def push(k):
+        f = frames[k % nf] if before_push is None else before_push(frames[k % nf])
+        rc = lib.cw_push_device(h, ctypes.c_void_p(f.data_ptr()), ctypes.byref(ready), ctypes.byref(fidx), sh)
+        if rc:
+            _native.check(rc, h)
+
+    k = 0
+    for _ in range(pipe.params.mz - 1 + warmup):
+        push(k)
+        k += 1
+    torch.cuda.synchronize()
+    lib.cw_set_timing(h, 1)
+    ms_tot, launches = ctypes.c_double(), ctypes.c_int64()
+    lib.cw_kernel_time(h, ctypes.byref(ms_tot), ctypes.byref(launches))
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(torch.cuda.current_device()) as clocks:
+        ev0.record(stream)
+        for _ in range(steps):
+            push(k)
+            k += 1
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    lib.cw_kernel_time(h, ctypes.byref(ms_tot), ctypes.byref(launches))
+    lib.cw_set_timing(h, 0)
+    return ev0.elapsed_time(ev1), ms_tot.value / max(1, launches.value), int(launches.value), clocks.summary()
+
+
+def run_config(args):
+    """--config c2 | c4 | c5: the other BASELINE.json configurations."""
+    import torch
+
+    from paper_1408_3526_b200 import FilterParams, Pipeline, _native, default_params
+    from paper_1408_3526_b200.scenegen import SimConfig, generate_device
+
+    world, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+    lib = _native.load()
+    peak, peak_kind = measured_peak()
+    lines = []
+
+    def maxrank(v):
+        if not dist:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t[0])
+
+    def line(metric, workload, px_per_step, p, elapsed, kern, launches, clocks, scaling, extra):
+        ms = maxrank(elapsed)
+        d = {"metric": metric, "value": px_per_step * args.steps / (ms / 1e3), "unit": UNIT, "n_gpus": world,
+             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+             "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f32",
+             "data": "synthetic (reference scene model, generated on device)",
+             "config": dict(workload=workload, **extra), "gpu_launches": args.steps,
+             "roofline": {"bound": "hbm", "achieved": b_alg(p) * px_per_step / world / (kern / 1e3) / 1e9,
+                          "peak": peak, "unit": "GB/s", "peak_kind": peak_kind,
+                          "frac": b_alg(p) * px_per_step / world / (kern / 1e3) / 1e9 / peak,
+                          "traffic": None, "bytes_per_px_frame": b_alg(p), "kernel_ms": kern,
+                          "launches_timed": launches},
+             "clocks": clocks}
+        lines.append(d)
+
+    if args.config == "c2":
+        w = h = 256
+        p = default_params()
+        frames = generate_device(SimConfig(width=w, height=h, frame_count=256, rng_seed=2 + rank), device=dev,
+                                 nonuniform=True)
+        with Pipeline(p, w, h, device=local) as pipe:
+            el, kern, n, clk = _device_run(lib, pipe, frames, args.steps, args.warmup, stream, dist)
+        line("pixel-frames/sec (256x256, non-uniform motion)", "C2: 256x256x256, non-uniform background motion",
+             w * h * world, p, el, kern, n, clk, "weak", {"frame": [w, h], "streams": world})
+    elif args.config == "c5":
+        w, h = 1280, 1024
+        frames = generate_device(SimConfig(width=w, height=h, frame_count=1000, rng_seed=rank), device=dev,
+                                 frames=16)
+        for name, kw in C5_SWEEP.items():
+            p = FilterParams(**kw)
+            with Pipeline(p, w, h, device=local) as pipe:
+                el, kern, n, clk = _device_run(lib, pipe, frames, args.steps, args.warmup, stream, dist)
+            line("pixel-frames/sec (1280x1024 stream per GPU, params sweep)", f"C5: {name}", w * h * world, p, el,
+                 kern, n, clk, "weak", {"frame": [w, h], "streams": world, "params": name})
+    elif args.config == "c4":
+        from paper_1408_3526_b200.strips import StripPipeline
+
+        w = h = 4096
+        p = default_params()
+        sp = StripPipeline(p, w, h, rank, world, device=local)
+        pl = sp.plan
+        own = generate_device(SimConfig(width=w, height=h, frame_count=200, rng_seed=4), device=dev, frames=6,
+                              rows=(pl.a0, pl.a1))
+        el, kern, n, clk = _device_run(lib, sp.pipe, own, args.steps, args.warmup, stream, dist,
+                                       before_push=sp.assemble)
+        sp.close()
+        line("pixel-frames/sec (4096x4096, strip-sharded)", "C4: 4096x4096, row strips + 8-row halo over NCCL",
+             w * h, p, el, kern, n, clk, "strong", {"frame": [w, h], "strips": world, "halo_rows": p.my - 1})
+    if rank == 0:
+        for d in lines:
+            print(json.dumps(d), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
@@ -370,11 +516,15 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU-oracle timing")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--config", choices=("c3", "c2", "c4", "c5"), default="c3",
+                    help="c3 (default, the headline) or another BASELINE.json configuration")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
     if args.impl == "reference":
         run_reference(args)
+    elif args.config != "c3":
+        run_config(args)
     else:
         run_ours(args)
 

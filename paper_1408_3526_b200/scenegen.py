@@ -118,26 +118,30 @@ def generate(cfg: SimConfig):
     return frames, comps
 
 
-def generate_device(cfg: SimConfig, device="cuda", nonuniform: bool = False, frames: int | None = None):
+def generate_device(cfg: SimConfig, device="cuda", nonuniform: bool = False, frames: int | None = None,
+                    rows: tuple[int, int] | None = None):
     """Same scene model evaluated on the GPU (torch float64), returns a
     (T, H, W) float32 CUDA tensor.  ``nonuniform`` applies the config-C2
-    motion field v(x, y) = (vx + 0.5 sin(2 pi y / H), vy + 0.375 cos(2 pi x / W))."""
+    motion field v(x, y) = (vx + 0.5 sin(2 pi y / H), vy + 0.375 cos(2 pi x / W)).
+    ``rows=(r0, r1)`` evaluates only image rows [r0, r1) (a strip of a large
+    frame, e.g. one rank's share of config C4); noise is drawn per strip."""
     import torch
 
     cfg.validate()
     rng = np.random.default_rng(cfg.rng_seed)
     comps = torch.tensor(_components(cfg, rng), dtype=torch.float64, device=device)
     n_frames = cfg.frame_count if frames is None else int(frames)
-    h, w = cfg.height, cfg.width
+    r0, r1 = rows if rows is not None else (0, cfg.height)
+    h, w = r1 - r0, cfg.width
     xs = torch.arange(w, dtype=torch.float64, device=device)[None, :]
-    ys = torch.arange(h, dtype=torch.float64, device=device)[:, None]
+    ys = torch.arange(r0, r1, dtype=torch.float64, device=device)[:, None]
     vx = torch.full((h, w), cfg.clutter_velocity[0], dtype=torch.float64, device=device)
     vy = torch.full((h, w), cfg.clutter_velocity[1], dtype=torch.float64, device=device)
     if nonuniform:
-        vx = vx + 0.5 * torch.sin(2 * math.pi * ys / h)
-        vy = vy + 0.375 * torch.cos(2 * math.pi * xs / w)
+        vx = vx + 0.5 * torch.sin(2 * math.pi * ys / cfg.height)
+        vy = vy + 0.375 * torch.cos(2 * math.pi * xs / cfg.width)
     gen = torch.Generator(device=device)
-    gen.manual_seed(cfg.rng_seed)
+    gen.manual_seed(cfg.rng_seed * 1000003 + r0)
     out = torch.empty((n_frames, h, w), dtype=torch.float32, device=device)
     for t in range(n_frames):
         acc = torch.full((h, w), cfg.dc_offset, dtype=torch.float64, device=device)
