@@ -133,6 +133,12 @@ int cw_push_inplace(cw_handle *h, int32_t *ready, int64_t *frame_index, void *st
 
 int64_t cw_frames_seen(const cw_handle *h);
 
+/* Spectrum backend (pipeline.py:139-142): 0 = recursive (sliding DFT +
+ * deadbeat observer, default), 1 = naive: every pixel's spectrum evaluated
+ * directly from its raw Mx x My x Mz window (spectrum.py:257-327), then the
+ * same conditioning, flow and PEF.  Switch before the first push. */
+int cw_set_backend(cw_handle *h, int32_t naive);
+
 /* Kept for ABI stability: the spectrum view (cw_read_view 0) is rebuilt
  * from the observer state, S = conj(w(kz)) z / sqrt(Mx My Mz); no flag needed. */
 int cw_set_debug(cw_handle *h, int32_t on);

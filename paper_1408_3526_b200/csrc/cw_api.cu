@@ -7,6 +7,7 @@
 // per function; there is no CPU compute path: every frame runs on the GPU
 // or the call fails with CW_ERR_CUDA.
 #include "cw_frame.cuh"
+#include "cw_naive.cuh"
 #include "../../include/cw_b200.h"
 
 #include <algorithm>
@@ -24,6 +25,9 @@ thread_local std::string g_create_error;
 
 struct LaunchFn {
     void (*launch)(const FrameArgs &, const Tables &, int grid, cudaStream_t);
+    void (*launch_naive)(const NaiveArgs &, const Tables &, int grid, cudaStream_t);
+    const void *naive_kernel;
+    size_t naive_smem;
     const void *kernel;
     int threads;
     size_t smem;
@@ -38,12 +42,23 @@ void launch_inst(const FrameArgs &a, const Tables &t, int grid, cudaStream_t s)
     cw_frame_kernel<G, NL><<<grid, G::NTHREADS, G::SMEM_BYTES, s>>>(a, t);
 }
 
+template <int KX, int KY, int KZ, int BX, int BY>
+void launch_naive_inst(const NaiveArgs &a, const Tables &t, int grid, cudaStream_t s)
+{
+    using G = Geo<KX, KY, KZ, BX, BY>;
+    constexpr size_t smem = sizeof(float) * (G::MZ * G::MY * (32 + G::MX - 1) + G::MZ * G::MY * G::XF * 32);
+    cw_naive_kernel<G><<<grid, G::NTHREADS, smem, s>>>(a, t);
+}
+
 template <int KX, int KY, int KZ, int BX, int BY, int NL>
 LaunchFn make_inst()
 {
     using G = Geo<KX, KY, KZ, BX, BY>;
     LaunchFn f;
     f.launch = &launch_inst<KX, KY, KZ, BX, BY, NL>;
+    f.launch_naive = &launch_naive_inst<KX, KY, KZ, BX, BY>;
+    f.naive_kernel = reinterpret_cast<const void *>(&cw_naive_kernel<G>);
+    f.naive_smem = sizeof(float) * (G::MZ * G::MY * (32 + G::MX - 1) + G::MZ * G::MY * G::XF * 32);
     f.kernel = reinterpret_cast<const void *>(&cw_frame_kernel<G, NL>);
     f.threads = G::NTHREADS;
     f.smem = G::SMEM_BYTES;
@@ -98,7 +113,9 @@ struct cw_handle {
     float *d_state = nullptr, *d_that = nullptr, *d_coef = nullptr, *d_frames = nullptr;
     float *d_res = nullptr, *d_pred = nullptr, *d_dbg = nullptr;  // 2 output sets each
     uint8_t *d_vidx = nullptr;
-    int nslots = 0;  // frame ring slots: mhat_z + 2 (one spare for the async upload)
+    int nslots = 0;  // frame ring slots: max(mhat_z + 2, Mz + 1) (async upload spare; naive window)
+    bool naive = false;  // spectrum backend: false = recursive (observer), true = naive window DFT
+    int naive_grid = 0;
     // async submit/wait (cw_submit): upload / download streams and per-frame events
     cudaStream_t up = nullptr, down = nullptr;
     static constexpr int NEV = 8;
@@ -446,13 +463,13 @@ int cw_create(const cw_params *p, int32_t width, int32_t height, int32_t device,
     if (cudaMalloc(&h->d_state, h->state_floats * 4) != cudaSuccess ||
         cudaMalloc(&h->d_that, h->that_floats * 4) != cudaSuccess ||
         cudaMalloc(&h->d_coef, coef.size() * 4) != cudaSuccess ||
-        cudaMalloc(&h->d_frames, HW * 4 * (h->mhz + 2)) != cudaSuccess ||
+        cudaMalloc(&h->d_frames, HW * 4 * std::max(h->mhz + 2, h->mz + 1)) != cudaSuccess ||
         cudaMalloc(&h->d_res, HW * 4 * 2) != cudaSuccess || cudaMalloc(&h->d_pred, HW * 4 * 2) != cudaSuccess ||
         cudaMalloc(&h->d_vidx, HW * 2 * 2) != cudaSuccess)
         return cleanup_fail(CW_ERR_NOMEM, "device allocation failed");
     cudaMemsetAsync(h->d_state, 0, h->state_floats * 4, h->own);
     cudaMemsetAsync(h->d_that, 0, h->that_floats * 4, h->own);
-    h->nslots = h->mhz + 2;
+    h->nslots = std::max(h->mhz + 2, h->mz + 1);
     cudaMemsetAsync(h->d_frames, 0, HW * 4 * h->nslots, h->own);
     cudaMemsetAsync(h->d_res, 0, HW * 4 * 2, h->own);
     cudaMemsetAsync(h->d_pred, 0, HW * 4 * 2, h->own);
@@ -594,6 +611,21 @@ static int run_frame(cw_handle *h, cudaStream_t s, int32_t *ready, int64_t *fram
         e1 = h->ev_pool[h->ev_used + 1];
         h->ev_used += 2;
         CW_CUDA(h, cudaEventRecord(e0, s));
+    }
+    if (h->naive && rd) {
+        // non-recursive spectrum of frames n-Mz+1 .. n into the state packets
+        NaiveArgs na;
+        na.frames = h->d_frames;
+        na.nslots = h->nslots;
+        na.n = n;
+        na.state = reinterpret_cast<float2 *>(h->d_state);
+        na.W = h->W;
+        na.H = h->H;
+        na.NXB = h->NXB;
+        na.y_begin = h->halo;
+        na.y_off = h->row_off;
+        h->fn.launch_naive(na, h->tab, h->naive_grid, s);
+        CW_CUDA(h, cudaGetLastError());
     }
     h->fn.launch(a, h->tab, h->grid, s);
     CW_CUDA(h, cudaGetLastError());
@@ -841,6 +873,24 @@ int cw_launch_info(const cw_handle *h, int32_t *kernels_per_push, int32_t *grid,
         *block = h->fn.threads;
     if (smem_bytes)
         *smem_bytes = (int32_t)h->fn.smem;
+    return CW_OK;
+}
+
+int cw_set_backend(cw_handle *h, int32_t naive)
+{
+    if (!h)
+        return CW_ERR_VALUE;
+    if (naive && !h->naive_grid) {
+        CW_CUDA(h, cudaSetDevice(h->device));
+        CW_CUDA(h, cudaFuncSetAttribute(h->fn.naive_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)h->fn.naive_smem));
+        int occ = 0, sms = 0;
+        CW_CUDA(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, h->fn.naive_kernel, h->fn.threads,
+                                                                 h->fn.naive_smem));
+        CW_CUDA(h, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
+        h->naive_grid = std::max(1, occ * sms);
+    }
+    h->naive = naive != 0;
     return CW_OK;
 }
 

@@ -10,8 +10,9 @@ call uploads the frame and runs ONE fused sm_100a kernel through the C ABI
 Differences from the reference, by design:
 * ``strategy`` is accepted and reported but never changes results (the
   device path has one execution shape).
-* ``spectrum_backend="naive"`` (the reference's non-recursive oracle
-  backend, spectrum.py:257-327) is not a device path yet and raises.
+* ``spectrum_backend="naive"`` (the reference's non-recursive backend,
+  spectrum.py:257-327) evaluates every pixel's window DFT directly on the
+  GPU (csrc/cw_naive.cuh) and feeds the same fused flow/PEF kernel.
 * ``imag_peak`` is 0.0 by construction: the PEF sums conjugate bin pairs,
   so the prediction is real without a discarded imaginary residue.
 """
@@ -177,9 +178,7 @@ class Pipeline:
             raise ParamError(
                 f"image {width}x{height} smaller than analysis window {params.mx}x{params.my}"
             )
-        if spectrum_backend == "naive":
-            raise ValueError("spectrum backend 'naive' has no device implementation yet")
-        if spectrum_backend != "recursive":
+        if spectrum_backend not in ("recursive", "naive"):
             raise ValueError(f"unknown spectrum backend {spectrum_backend!r}")
         self.spectrum_backend = spectrum_backend
         if bank is None:
@@ -223,6 +222,8 @@ class Pipeline:
         self._h = handle
         if self._forced is not None:
             _native.check(lib.cw_set_forced_velocity(self._h, *self._forced), self._h)
+        if spectrum_backend == "naive":
+            _native.check(lib.cw_set_backend(self._h, 1), self._h)
         self._detect = detect_threshold is not None
         self._max_det = int(max_detections)
         if self._detect:

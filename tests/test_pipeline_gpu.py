@@ -308,3 +308,24 @@ def test_detection_epilogue_matches_host_metrics(params, stream):
         assert np.array_equal(o.detections[:, 0].astype(int), xs)
         assert np.array_equal(o.detections[:, 1].astype(int), ys)
         assert np.array_equal(o.detections[:, 2].astype(np.float32), o.residual[ys, xs])
+
+
+def test_naive_backend_matches_recursive(params):
+    """test_pipeline.py:131-139: the non-recursive spectrum backend gives the
+    recursive pipeline's outputs (residual 1e-5, identical velocity bins)."""
+    rng = np.random.default_rng(47)
+    frames = rng.random((8, 14, 14)).astype(np.float32)
+    rec, _, _ = _run_gpu(params, frames, spectrum_backend="recursive")
+    nai, _, _ = _run_gpu(params, frames, spectrum_backend="naive")
+    assert len(rec) == len(nai) == 4
+    for a, b in zip(rec, nai):
+        assert np.abs(a.residual - b.residual).max() < 1e-5
+        assert np.array_equal(a.velocity.indices, b.velocity.indices)
+
+
+def test_naive_backend_vs_oracle(params):
+    from paper_1408_3526_b200.scenegen import SimConfig, generate
+
+    frames, _ = generate(SimConfig(width=72, height=40, frame_count=12, rng_seed=8))
+    gpu, specs, _ = _run_gpu(params, frames, spectrum_backend="naive", spectrum_at=(11,))
+    _compare(params, frames, gpu, _run_oracle(params, frames))
