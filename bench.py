@@ -487,6 +487,17 @@ def run_config(args):
                 el, kern, n, clk = _device_run(lib, pipe, frames, args.steps, args.warmup, stream, dist)
             line("pixel-frames/sec (1280x1024 stream per GPU, params sweep)", f"C5: {name}", w * h * world, p, el,
                  kern, n, clk, "weak", {"frame": [w, h], "streams": world, "params": name})
+    elif args.config == "c3naive":
+        # the paper's naive-vs-recursive comparison at 640x512
+        p = default_params()
+        frames = generate_device(SimConfig(width=WIDTH, height=HEIGHT, frame_count=1000, rng_seed=rank),
+                                 device=dev, frames=32)
+        for backend in ("recursive", "naive"):
+            with Pipeline(p, WIDTH, HEIGHT, device=local, spectrum_backend=backend) as pipe:
+                el, kern, n, clk = _device_run(lib, pipe, frames, args.steps, args.warmup, stream, dist)
+            line("pixel-frames/sec (640x512, full pipeline)", f"C3 with spectrum_backend={backend}",
+                 WIDTH * HEIGHT * world, p, el, kern, n, clk, "weak",
+                 {"frame": [WIDTH, HEIGHT], "spectrum_backend": backend})
     elif args.config == "c4":
         from paper_1408_3526_b200.strips import StripPipeline
 
@@ -516,7 +527,7 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU-oracle timing")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--config", choices=("c3", "c2", "c4", "c5"), default="c3",
+    ap.add_argument("--config", choices=("c3", "c2", "c4", "c5", "c3naive"), default="c3",
                     help="c3 (default, the headline) or another BASELINE.json configuration")
     args = ap.parse_args()
     if args.warmup < 3:
