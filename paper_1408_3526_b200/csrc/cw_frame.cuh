@@ -37,6 +37,7 @@ namespace cwb {
 constexpr int MAXK = 5;    // largest half window supported by the tables
 constexpr int MAXM = 2 * MAXK + 1;
 constexpr int MAXL = 33;   // largest lag grid per axis
+constexpr int LREC = (1 + 2 * MAXK + 3) / 4 * 4;  // floats per lag coefficient record
 constexpr int RESTART = 32;  // rows between direct y-SDFT restarts (bounds f32 drift)
 #ifndef CW_FENCE_ALL
 #define CW_FENCE_ALL 1  // every thread orders its generic stage reads before the next TMA write
@@ -54,10 +55,12 @@ struct Tables {
     // kz collapse a_z(kz) = exp(-j 2 pi kz / Mz), index kz + KZ, times
     // norm^2 / 4096 (the three unscaled Hann passes each carry a factor 4)
     float azc[MAXM], azs[MAXM];
+    // lag-contraction coefficients, one 16-byte aligned record per lag:
+    // [0] = gain, [1..MAXK] = cos terms, [MAXK+1..2 MAXK] = sin terms.
     // stage 1 (gx folded): B(ky,lx) = g*T(0) + sum_kx c*A - j s*D
-    float s1g[MAXL], s1c[MAXL][MAXK], s1s[MAXL][MAXK];
-    // stage 2 (gy and the factor 2 folded)
-    float s2g[MAXL], s2c[MAXL][MAXK], s2s[MAXL][MAXK];
+    // stage 2 (gy and the factor 2 folded): R = g B0 + sum_ky c Re B + s Im B
+    alignas(16) float s1v[MAXL][LREC];
+    alignas(16) float s2v[MAXL][LREC];
     // argmax total order: rank[ly * nlx + lx]; rank -> (ix, iy)
     uint16_t rank[MAXL * MAXL];
     uint8_t rix[MAXL * MAXL], riy[MAXL * MAXL];
@@ -655,17 +658,17 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                         // interleaved chains (q odd / even) for ILP, each strict '>',
                         // merged by visit index -> the reference's tie winner
                         constexpr int C0 = NL / 2;
-                        float ca = -INFINITY, cb = t.s2g[C0] * b0;
+                        float ca = -INFINITY, cb = t.s2v[C0][0] * b0;
 #pragma unroll
-                        for (int k = 1; k <= KY; k++) cb = fmaf(t.s2c[C0][k - 1], br[k], cb);
+                        for (int k = 1; k <= KY; k++) cb = fmaf(t.s2v[C0][k], br[k], cb);
                         int ia = 0x7fff, ib = 0;
 #pragma unroll
                         for (int q = 1; q <= C0; q++) {
-                            float e = t.s2g[C0 + q] * b0, o = 0.f;
+                            float e = t.s2v[C0 + q][0] * b0, o = 0.f;
 #pragma unroll
                             for (int k = 1; k <= KY; k++) {
-                                e = fmaf(t.s2c[C0 + q][k - 1], br[k], e);
-                                o = fmaf(t.s2s[C0 + q][k - 1], bi[k], o);
+                                e = fmaf(t.s2v[C0 + q][k], br[k], e);
+                                o = fmaf(t.s2v[C0 + q][MAXK + k], bi[k], o);
                             }
                             const float vm = e - o, vp = e + o;
                             if (q & 1) {
@@ -682,11 +685,11 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                         if (better(cb, rk, best, brk)) { best = cb; brk = rk; }
                     } else {
                         for (int ly = 0; ly < nly; ly++) {
-                            float v = t.s2g[ly] * b0;
+                            float v = t.s2v[ly][0] * b0;
 #pragma unroll
                             for (int k = 1; k <= KY; k++) {
-                                v = fmaf(t.s2c[ly][k - 1], br[k], v);
-                                v = fmaf(t.s2s[ly][k - 1], bi[k], v);
+                                v = fmaf(t.s2v[ly][k], br[k], v);
+                                v = fmaf(t.s2v[ly][MAXK + k], bi[k], v);
                             }
                             const int rk = srank[ly * nlx + lx];
                             if (better(v, rk, best, brk)) { best = v; brk = rk; }
@@ -698,12 +701,12 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                     constexpr int C0 = NL / 2;
                     for (int q = r; q <= C0; q += NR) {
                         const int lp = C0 + q;
-                        const float g = t.s1g[lp];
+                        const float g = t.s1v[lp][0];
                         float c1[KX + 1], s1[KX + 1];
 #pragma unroll
                         for (int kx = 1; kx <= KX; kx++) {
-                            c1[kx] = t.s1c[lp][kx - 1];
-                            s1[kx] = t.s1s[lp][kx - 1];
+                            c1[kx] = t.s1v[lp][kx];
+                            s1[kx] = t.s1v[lp][MAXK + kx];
                         }
                         float bp0, bm0, brp[KY + 1], bip[KY + 1], brm[KY + 1], bim[KY + 1];
                         {   // row 0: T(0,-kx) = conj T(0,kx)
@@ -740,15 +743,15 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                     }
                 } else {
                     for (int lx = r; lx < nlx; lx += NR) {
-                        const float g = t.s1g[lx];
+                        const float g = t.s1v[lx][0];
                         float b0, br[KY + 1], bi[KY + 1];
                         {
                             float b = g * tv(0, 0).r;
 #pragma unroll
                             for (int kx = 1; kx <= KX; kx++) {
                                 const cf v = tv(0, kx);
-                                b = fmaf(2.f * t.s1c[lx][kx - 1], v.r, b);
-                                b = fmaf(2.f * t.s1s[lx][kx - 1], v.i, b);
+                                b = fmaf(2.f * t.s1v[lx][kx], v.r, b);
+                                b = fmaf(2.f * t.s1v[lx][MAXK + kx], v.i, b);
                             }
                             b0 = b;
                         }
@@ -760,7 +763,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                             for (int kx = 1; kx <= KX; kx++) {
                                 const cf tp = tv(ky, kx), tm = tv(ky, -kx);
                                 const cf A = cadd(tp, tm), D = csub(tp, tm);
-                                const float c = t.s1c[lx][kx - 1], s = t.s1s[lx][kx - 1];
+                                const float c = t.s1v[lx][kx], s = t.s1v[lx][MAXK + kx];
                                 xr = fmaf(c, A.r, fmaf(s, D.i, xr));
                                 xi = fmaf(c, A.i, fmaf(-s, D.r, xi));
                             }
