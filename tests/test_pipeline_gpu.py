@@ -329,3 +329,23 @@ def test_naive_backend_vs_oracle(params):
     frames, _ = generate(SimConfig(width=72, height=40, frame_count=12, rng_seed=8))
     gpu, specs, _ = _run_gpu(params, frames, spectrum_backend="naive", spectrum_at=(11,))
     _compare(params, frames, gpu, _run_oracle(params, frames))
+
+
+@pytest.mark.parametrize("kw", [
+    dict(lag_grid_x=(-1.0, -0.5, 0.25, 1.0, 1.75), lag_grid_y=(-1.25, 0.0, 0.5)),    # asymmetric grids
+    dict(lag_grid_x=tuple(i / 4 - 0.125 for i in range(-7, 9)),                     # even length, no 0
+         lag_grid_y=tuple(i / 4 - 0.125 for i in range(-7, 9))),
+    dict(mhat=(0, 0, 0)),
+    dict(mhat=(8, 8, 4)),
+    dict(mhat=(2, 6, 1), alpha=0.5),
+])
+def test_parameter_variants_vs_oracle(kw):
+    """The runtime-loop contraction (non-symmetric / even lag grids) and the
+    output placement for other group delays, against the oracle."""
+    from paper_1408_3526_b200 import FilterParams
+    from paper_1408_3526_b200.scenegen import SimConfig, generate
+
+    p = FilterParams(**kw)
+    frames, _ = generate(SimConfig(width=70, height=45, frame_count=11, rng_seed=21))
+    gpu, _, _ = _run_gpu(p, frames)
+    _compare(p, frames, gpu, _run_oracle(p, frames))
