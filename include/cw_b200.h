@@ -121,6 +121,17 @@ int cw_wait(cw_handle *h, int64_t ticket, int32_t *ready, int64_t *frame_index);
 int cw_set_detection(cw_handle *h, float tau, int32_t cap);
 int cw_detections(cw_handle *h, int64_t ticket, int32_t *n_total, float *xyr, int32_t out_cap, double *stats);
 
+/*
+ * Checkpoint / resume: the complete stream state (observer state, smoothing
+ * state T^, raw-frame ring, frame counter) as one host blob of
+ * cw_snapshot_size() bytes.  cw_restore() into a pipeline of the same
+ * geometry continues the stream exactly where the snapshot was taken (no
+ * new warm-up; the reference can only restart, pipeline.py:245-247).
+ */
+int cw_snapshot_size(const cw_handle *h, size_t *bytes);
+int cw_snapshot(cw_handle *h, void *dst, size_t bytes);
+int cw_restore(cw_handle *h, const void *src, size_t bytes);
+
 /* Synchronous device -> host copy (e.g. of cw_device_outputs buffers). */
 int cw_copy_to_host(cw_handle *h, void *dst, const void *src_dev, size_t bytes);
 

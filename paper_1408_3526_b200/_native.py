@@ -34,7 +34,7 @@ EXPORTS = (
     "cw_push", "cw_push_device", "cw_device_outputs", "cw_next_frame_slot", "cw_push_inplace",
     "cw_frames_seen", "cw_set_debug", "cw_read_view", "cw_launch_info", "cw_set_timing",
     "cw_kernel_time", "cw_copy_to_host", "cw_submit", "cw_wait", "cw_set_detection", "cw_detections",
-    "cw_set_backend",
+    "cw_set_backend", "cw_snapshot_size", "cw_snapshot", "cw_restore",
 )
 
 
@@ -105,6 +105,9 @@ def load():
         "cw_wait": (ctypes.c_int, [vp, i64, P(i32), P(i64)]),
         "cw_set_detection": (ctypes.c_int, [vp, ctypes.c_float, i32]),
         "cw_set_backend": (ctypes.c_int, [vp, i32]),
+        "cw_snapshot_size": (ctypes.c_int, [vp, P(ctypes.c_size_t)]),
+        "cw_snapshot": (ctypes.c_int, [vp, vp, ctypes.c_size_t]),
+        "cw_restore": (ctypes.c_int, [vp, vp, ctypes.c_size_t]),
         "cw_detections": (ctypes.c_int, [vp, i64, P(i32), P(ctypes.c_float), i32, P(ctypes.c_double)]),
         "cw_kernel_time": (ctypes.c_int, [vp, P(ctypes.c_double), P(i64)]),
     }

@@ -852,6 +852,69 @@ extern "C" int cw_phase_clocks(unsigned long long *dst)  // [8][16], then zeroed
 }
 #endif
 
+// Checkpoint / resume: the whole stream state -- observer
+// state, T^, frame ring, counters -- as one host blob.
+struct SnapHeader {
+    uint64_t magic, version;
+    int64_t frames_seen;
+    int32_t have_that, W, H, kx, ky, kz, nslots, pad;
+    uint64_t state_bytes, that_bytes, frames_bytes;
+};
+static const uint64_t SNAP_MAGIC = 0x43574232534e4150ull;  // "CWB2SNAP"
+
+int cw_snapshot_size(const cw_handle *h, size_t *bytes)
+{
+    if (!h || !bytes)
+        return CW_ERR_VALUE;
+    *bytes = sizeof(SnapHeader) + (h->state_floats + h->that_floats) * 4 + (size_t)h->W * h->H * 4 * h->nslots;
+    return CW_OK;
+}
+
+int cw_snapshot(cw_handle *h, void *dst, size_t bytes)
+{
+    size_t need = 0;
+    cw_snapshot_size(h, &need);
+    if (!h || !dst || bytes != need)
+        return h ? fail(h, CW_ERR_VALUE, "snapshot buffer size mismatch") : CW_ERR_VALUE;
+    CW_CUDA(h, cudaSetDevice(h->device));
+    CW_CUDA(h, cudaDeviceSynchronize());
+    SnapHeader hd{SNAP_MAGIC, 1, h->frames_seen, h->have_that ? 1 : 0, h->W, h->H, h->kx, h->ky, h->kz, h->nslots, 0,
+                  h->state_floats * 4, h->that_floats * 4, (size_t)h->W * h->H * 4 * h->nslots};
+    unsigned char *o = static_cast<unsigned char *>(dst);
+    std::memcpy(o, &hd, sizeof hd);
+    o += sizeof hd;
+    CW_CUDA(h, cudaMemcpy(o, h->d_state, hd.state_bytes, cudaMemcpyDeviceToHost));
+    o += hd.state_bytes;
+    CW_CUDA(h, cudaMemcpy(o, h->d_that, hd.that_bytes, cudaMemcpyDeviceToHost));
+    o += hd.that_bytes;
+    CW_CUDA(h, cudaMemcpy(o, h->d_frames, hd.frames_bytes, cudaMemcpyDeviceToHost));
+    return CW_OK;
+}
+
+int cw_restore(cw_handle *h, const void *src, size_t bytes)
+{
+    size_t need = 0;
+    cw_snapshot_size(h, &need);
+    if (!h || !src || bytes != need)
+        return h ? fail(h, CW_ERR_VALUE, "snapshot size does not match this pipeline") : CW_ERR_VALUE;
+    SnapHeader hd;
+    std::memcpy(&hd, src, sizeof hd);
+    if (hd.magic != SNAP_MAGIC || hd.version != 1 || hd.W != h->W || hd.H != h->H || hd.kx != h->kx ||
+        hd.ky != h->ky || hd.kz != h->kz || hd.nslots != h->nslots)
+        return fail(h, CW_ERR_VALUE, "snapshot was taken from a different pipeline geometry");
+    CW_CUDA(h, cudaSetDevice(h->device));
+    CW_CUDA(h, cudaDeviceSynchronize());
+    const unsigned char *p = static_cast<const unsigned char *>(src) + sizeof hd;
+    CW_CUDA(h, cudaMemcpy(h->d_state, p, hd.state_bytes, cudaMemcpyHostToDevice));
+    p += hd.state_bytes;
+    CW_CUDA(h, cudaMemcpy(h->d_that, p, hd.that_bytes, cudaMemcpyHostToDevice));
+    p += hd.that_bytes;
+    CW_CUDA(h, cudaMemcpy(h->d_frames, p, hd.frames_bytes, cudaMemcpyHostToDevice));
+    h->frames_seen = hd.frames_seen;
+    h->have_that = hd.have_that != 0;
+    return CW_OK;
+}
+
 int cw_copy_to_host(cw_handle *h, void *dst, const void *src_dev, size_t bytes)
 {
     if (!h || !dst || !src_dev)

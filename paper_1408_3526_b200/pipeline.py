@@ -385,6 +385,23 @@ class Pipeline:
         }
         return det, metrics
 
+    # -- checkpoint / resume -----------------------------------------------
+
+    def snapshot(self) -> np.ndarray:
+        """The whole stream state (observer + smoothing state, frame ring,
+        counters) as a uint8 array; ``restore`` continues from it."""
+        lib = _native.load()
+        n = ctypes.c_size_t(0)
+        _native.check(lib.cw_snapshot_size(self._h, ctypes.byref(n)), self._h)
+        buf = np.empty(n.value, np.uint8)
+        _native.check(lib.cw_snapshot(self._h, buf.ctypes.data, buf.nbytes), self._h)
+        return buf
+
+    def restore(self, snap) -> None:
+        """Resume from ``snapshot()`` of a pipeline with the same geometry."""
+        snap = np.ascontiguousarray(snap, dtype=np.uint8)
+        _native.check(_native.load().cw_restore(self._h, snap.ctypes.data, snap.nbytes), self._h)
+
     # -- parity views (tests) ------------------------------------------------
 
     def enable_spectrum_dump(self, on: bool = True) -> None:

@@ -349,3 +349,28 @@ def test_parameter_variants_vs_oracle(kw):
     frames, _ = generate(SimConfig(width=70, height=45, frame_count=11, rng_seed=21))
     gpu, _, _ = _run_gpu(p, frames)
     _compare(p, frames, gpu, _run_oracle(p, frames))
+
+
+def test_snapshot_restore_resumes_exactly(params):
+    """Checkpoint after frame 7, restore into a fresh pipeline: frames 8.. give
+    bit-identical outputs to the uninterrupted run (no new warm-up)."""
+    from paper_1408_3526_b200 import Pipeline
+
+    rng = np.random.default_rng(5)
+    frames = (10 + rng.standard_normal((14, 40, 70))).astype(np.float32)
+    full, _, _ = _run_gpu(params, frames)
+    with Pipeline(params, 70, 40) as a:
+        for f in frames[:8]:
+            a.process_frame(f)
+        snap = a.snapshot()
+    with Pipeline(params, 70, 40) as b:
+        b.restore(snap)
+        assert b.frames_seen == 8
+        resumed = [b.process_frame(f) for f in frames[8:]]
+    for x, y in zip(full[-6:], resumed):
+        assert y is not None and x.frame_index == y.frame_index
+        assert np.array_equal(x.residual, y.residual)
+        assert np.array_equal(x.velocity.indices, y.velocity.indices)
+    with Pipeline(params, 71, 40) as c:
+        with pytest.raises(ValueError):
+            c.restore(snap)
