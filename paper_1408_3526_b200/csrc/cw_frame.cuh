@@ -775,18 +775,21 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                 }
                 pbest[r * 32 + lane] = make_float2(best, __int_as_float(brk));
             }
+            // warp KY (fewest lag columns, no PEF): x stage of yy+1 from the
+            // row segment it prefetched in C1; barrier 3 orders it before any
+            // consumer in the next phase B
+            if (r == KY && yy + 1 < ye) {
+                cp_async_wait_all();
+                __syncwarp();
+                xstage_s(ring_slot(yy + 1));
+            }
             if (CW_FENCE_ALL) fence_proxy_async();  // T^ stage reads before the next TMA write
             CW_STAMP(7);  // CD
             __syncthreads();  // (3) partial maxima visible; the T^ stage is free
             CW_STAMP(8);  // barrier 3 wait
             if (yy + 1 < ye) issue_t(yy + 1, xb);
 
-            // ---------------- phase E: final pick, PEF partials; x stage of yy+1 ----------------
-            if (r == KY && yy + 1 < ye) {
-                cp_async_wait_all();
-                __syncwarp();
-                xstage_s(ring_slot(yy + 1));
-            }
+            // ---------------- phase E: final pick, PEF partials ----------------
             int vix, viy;
             {
                 const float2 bv = pbest[lane];
@@ -832,7 +835,9 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                 *reinterpret_cast<uchar2 *>(vp) = make_uchar2((uint8_t)vix, (uint8_t)viy);
             }
             CW_STAMP(9);  // E
-            __syncthreads();  // (4) PEF partials visible
+            // (4) PEF partials visible to warp 0 -- only the PEF warps 0..BY
+            // meet here; warp KY runs on into the next row's phase B
+            if (r <= BY) asm volatile("bar.sync 1, %0;" ::"n"((BY + 1) * 32) : "memory");
             CW_STAMP(10);  // barrier 4 wait
 
             // ---------------- phase F: residual (+ threshold epilogue) ----------------
