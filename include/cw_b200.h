@@ -150,10 +150,6 @@ int64_t cw_frames_seen(const cw_handle *h);
  * same conditioning, flow and PEF.  Switch before the first push. */
 int cw_set_backend(cw_handle *h, int32_t naive);
 
-/* Kept for ABI stability: the spectrum view (cw_read_view 0) is rebuilt
- * from the observer state, S = conj(w(kz)) z / sqrt(Mx My Mz); no flag needed. */
-int cw_set_debug(cw_handle *h, int32_t on);
-
 /*
  * Parity views (tests only), copied to host after synchronising:
  *  what = 0: spectrum S of the last frame, (H, W, Mz, My, Mx) complex128

@@ -32,7 +32,7 @@ CW_OK, CW_ERR_PARAM, CW_ERR_VALUE, CW_ERR_CUDA, CW_ERR_NOMEM, CW_ERR_UNSUPPORTED
 EXPORTS = (
     "cw_abi_version", "cw_create", "cw_destroy", "cw_last_error", "cw_set_forced_velocity",
     "cw_push", "cw_push_device", "cw_device_outputs", "cw_next_frame_slot", "cw_push_inplace",
-    "cw_frames_seen", "cw_set_debug", "cw_read_view", "cw_launch_info", "cw_set_timing",
+    "cw_frames_seen", "cw_read_view", "cw_launch_info", "cw_set_timing",
     "cw_kernel_time", "cw_copy_to_host", "cw_submit", "cw_wait", "cw_set_detection", "cw_detections",
     "cw_set_backend", "cw_snapshot_size", "cw_snapshot", "cw_restore",
 )
@@ -95,7 +95,6 @@ def load():
         "cw_next_frame_slot": (ctypes.c_int, [vp, P(vp)]),
         "cw_push_inplace": (ctypes.c_int, [vp, P(i32), P(i64), vp]),
         "cw_frames_seen": (i64, [vp]),
-        "cw_set_debug": (ctypes.c_int, [vp, i32]),
         "cw_read_view": (ctypes.c_int, [vp, i32, vp, ctypes.c_size_t]),
         "cw_launch_info": (ctypes.c_int, [vp, P(i32), P(i32), P(i32), P(i32)]),
         "cw_set_timing": (ctypes.c_int, [vp, i32]),

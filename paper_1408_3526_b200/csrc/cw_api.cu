@@ -111,7 +111,7 @@ struct cw_handle {
     int grid;
     cudaStream_t own = nullptr;
     float *d_state = nullptr, *d_that = nullptr, *d_coef = nullptr, *d_frames = nullptr;
-    float *d_res = nullptr, *d_pred = nullptr, *d_dbg = nullptr;  // 2 output sets each
+    float *d_res = nullptr, *d_pred = nullptr;  // 2 output sets each
     uint8_t *d_vidx = nullptr;
     int nslots = 0;  // frame ring slots: max(mhat_z + 2, Mz + 1) (async upload spare; naive window)
     bool naive = false;  // spectrum backend: false = recursive (observer), true = naive window DFT
@@ -132,7 +132,6 @@ struct cw_handle {
     size_t state_floats = 0, that_floats = 0;  // floats (pairs x 2)
     long long frames_seen = 0;
     bool have_that = false;
-    bool debug = false;
     int forced_ix = -1, forced_iy = -1;
     // optional per-launch timing: events recorded around each frame kernel
     bool timing = false;
@@ -502,7 +501,6 @@ void cw_destroy(cw_handle *h)
     cudaFree(h->d_res);
     cudaFree(h->d_pred);
     cudaFree(h->d_vidx);
-    cudaFree(h->d_dbg);
     cudaFree(h->d_det);
     if (h->h_det)
         cudaFreeHost(h->h_det);
@@ -538,14 +536,6 @@ int cw_set_forced_velocity(cw_handle *h, int32_t ix, int32_t iy)
         return fail(h, CW_ERR_PARAM, "forced velocity index outside the grid");
     h->forced_ix = ix;
     h->forced_iy = iy;
-    return CW_OK;
-}
-
-int cw_set_debug(cw_handle *h, int32_t on)
-{
-    if (!h)
-        return CW_ERR_VALUE;
-    h->debug = on != 0;  // the spectrum view is rebuilt from the observer state
     return CW_OK;
 }
 

@@ -404,13 +404,9 @@ class Pipeline:
 
     # -- parity views (tests) ------------------------------------------------
 
-    def enable_spectrum_dump(self, on: bool = True) -> None:
-        """Record the observer spectrum S of each frame (tests/parity only)."""
-        _native.check(_native.load().cw_set_debug(self._h, int(bool(on))), self._h)
-
     def spectrum(self) -> np.ndarray:
         """S of the last frame as (H, W, Mz, My, Mx) complex128 (reference
-        SpectrumField.bins layout); needs enable_spectrum_dump() first."""
+        SpectrumField.bins layout), rebuilt from the observer state."""
         p = self.params
         out = np.zeros((self.height, self.width, p.mz, p.my, p.mx), np.complex128)
         rc = _native.load().cw_read_view(self._h, 0, out.ctypes.data, out.nbytes)

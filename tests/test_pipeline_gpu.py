@@ -20,8 +20,6 @@ def _run_gpu(params, frames, forced=None, bank=None, spectrum_at=(), **kw):
     t, h, w = frames.shape
     outs, specs, thats = [], {}, {}
     with Pipeline(params, w, h, forced_velocity=forced, bank=bank, **kw) as pipe:
-        if spectrum_at:
-            pipe.enable_spectrum_dump()
         for n in range(t):
             o = pipe.process_frame(frames[n])
             if o is not None:

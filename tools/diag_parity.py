@@ -14,7 +14,6 @@ frames = z["frames"]
 fmax = np.abs(frames).max()
 y0, y1, x0, x1 = (int(v) for v in z["crop_box"])
 with Pipeline(p, 64, 64) as pipe:
-    pipe.enable_spectrum_dump()
     k = 0
     for n in range(32):
         o = pipe.process_frame(frames[n])
