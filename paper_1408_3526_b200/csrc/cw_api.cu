@@ -10,6 +10,8 @@
 #include "cw_naive.cuh"
 #include "../../include/cw_b200.h"
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX ranges (visible in nsys / ncu --nvtx)
+
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -556,8 +558,14 @@ static cudaStream_t pick_stream(cw_handle *h, void *stream)
 }
 
 // The frame already sits in its ring slot: run the fused kernel.
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
 static int run_frame(cw_handle *h, cudaStream_t s, int32_t *ready, int64_t *frame_index)
 {
+    NvtxRange nvtx("cw_frame");
     const size_t HW = (size_t)h->W * h->H;
     const long long n = h->frames_seen;
     const int rd = (n + 1 >= h->mz) ? 1 : 0;
@@ -658,6 +666,7 @@ int cw_push_device(cw_handle *h, const float *frame_dev, int32_t *ready, int64_t
 int cw_push(cw_handle *h, const float *frame, float *residual, float *prediction, uint8_t *vidx, int32_t *ready,
             int64_t *frame_index, void *stream)
 {
+    NvtxRange nvtx("cw_push");
     if (!h || !frame)
         return CW_ERR_VALUE;
     cudaStream_t s = pick_stream(h, stream);
@@ -716,6 +725,7 @@ int cw_device_outputs(cw_handle *h, float **residual, float **prediction, uint8_
 int cw_submit(cw_handle *h, const float *frame, float *residual, float *prediction, uint8_t *vidx,
               int64_t *ticket)
 {
+    NvtxRange nvtx("cw_submit");
     if (!h || !frame || !ticket)
         return CW_ERR_VALUE;
     const size_t HW = (size_t)h->W * h->H;

@@ -168,6 +168,7 @@ class Pipeline:
         device: int = 0,
         detect_threshold: float | None = None,
         max_detections: int = 65536,
+        device_timing: bool = False,
         _strip: tuple[int, int] = (0, 0),
     ):
         validate(params)
@@ -224,6 +225,9 @@ class Pipeline:
             _native.check(lib.cw_set_forced_velocity(self._h, *self._forced), self._h)
         if spectrum_backend == "naive":
             _native.check(lib.cw_set_backend(self._h, 1), self._h)
+        self._device_timing = bool(device_timing)
+        if self._device_timing:  # kernel milliseconds in last_timings (CUDA events)
+            _native.check(lib.cw_set_timing(self._h, 1), self._h)
         self._detect = detect_threshold is not None
         self._max_det = int(max_detections)
         if self._detect:
@@ -270,6 +274,10 @@ class Pipeline:
         )
         _native.check(rc, self._h)
         self.last_timings = {"pipeline": time.perf_counter() - t0}
+        if self._device_timing:
+            ms, n = ctypes.c_double(), ctypes.c_int64()
+            _native.check(lib.cw_kernel_time(self._h, ctypes.byref(ms), ctypes.byref(n)), self._h)
+            self.last_timings["kernel"] = ms.value / 1e3
         if not ready.value:
             return None
         return self._wrap(int(fidx.value), res, pred, vidx, ticket=self.frames_seen - 1)

@@ -372,3 +372,14 @@ def test_snapshot_restore_resumes_exactly(params):
     with Pipeline(params, 71, 40) as c:
         with pytest.raises(ValueError):
             c.restore(snap)
+
+
+def test_device_timing_reported(params):
+    from paper_1408_3526_b200 import Pipeline
+
+    rng = np.random.default_rng(6)
+    with Pipeline(params, 64, 48, device_timing=True) as pipe:
+        for f in (10 + rng.standard_normal((7, 48, 64))).astype(np.float32):
+            pipe.process_frame(f)
+        t = pipe.last_timings
+    assert 0 < t["kernel"] <= t["pipeline"]
