@@ -164,6 +164,10 @@ struct Geo {
     static constexpr int SM_BAR = 16;
     static constexpr size_t SMEM_BYTES =
         SM_STAGE + SM_TSTAGE + SM_RET + SM_XF + SM_BEST + SM_PEF + SM_RANK + SM_ROW + SM_DEL + SM_BAR;
+    // resident CTAs per SM the register budget is sized for: as many as the
+    // 228 KB of shared memory hold (1 KB reserved per CTA), at most 3
+    static constexpr int MINB_SMEM = (int)((228 * 1024) / (SMEM_BYTES + 1024));
+    static constexpr int MINB = MINB_SMEM < 1 ? 1 : (MINB_SMEM > 3 ? 3 : MINB_SMEM);
 };
 
 struct cf {
@@ -247,7 +251,7 @@ __device__ __forceinline__ void cp_async4(void *dst, const float *src, bool vali
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 template <class G, int NL>
-__global__ void __launch_bounds__(G::NTHREADS, 2)
+__global__ void __launch_bounds__(G::NTHREADS, G::MINB)
 cw_frame_kernel(const FrameArgs a, const Tables t)
 {
 #ifdef CW_PHASE_TIMING
