@@ -26,10 +26,10 @@ template <class G>
 __global__ void __launch_bounds__(G::NTHREADS, 1)
 cw_naive_kernel(const NaiveArgs a, const Tables t)
 {
-    constexpr int KX = G::KX, KY = G::KY, KZ = G::KZ;
+    constexpr int KX = G::KX, KZ = G::KZ;
     constexpr int MX = G::MX, MY = G::MY, MZ = G::MZ, NR = G::NR;
     constexpr int SW = 32 + MX - 1;  // staged columns per row
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     float *samp = reinterpret_cast<float *>(smem_raw);  // [MZ][MY][SW]
     float *xf = samp + MZ * MY * SW;                     // [MZ][MY][XF][32]
 
