@@ -107,6 +107,20 @@ int cw_submit(cw_handle *h, const float *frame, float *residual, float *predicti
 int cw_wait(cw_handle *h, int64_t ticket, int32_t *ready, int64_t *frame_index);
 
 /*
+ * cw_submit for a frame in a sequence-file sample format (replaces the host
+ * decode of read_sequence, seqio.py:172-204; the payloads of seqio.py:1-8):
+ *   CW_FMT_F32LE: little-endian float32 (frames.f32), scale/offset ignored;
+ *   CW_FMT_PGM16: P5 payload, big-endian uint16 q; the frame is
+ *                 f32(f64(q) * scale + offset), byte-swapped and de-quantised
+ *                 on the device (half the upload bytes of float32).
+ * `samples` = H*W samples (the PGM payload after its header).
+ */
+#define CW_FMT_F32LE 0
+#define CW_FMT_PGM16 1
+int cw_submit_raw(cw_handle *h, const void *samples, int32_t format, double scale, double offset,
+                  float *residual, float *prediction, uint8_t *vidx, int64_t *ticket);
+
+/*
  * Fused detection epilogue ("final threshold"; the truth-free
  * metrics of cli.compute_metrics_row, cli.py:157-208).  cw_set_detection(h,
  * tau, cap): every valid output pixel with |residual| >= tau (tau <= 0: no

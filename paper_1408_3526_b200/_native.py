@@ -33,9 +33,12 @@ EXPORTS = (
     "cw_abi_version", "cw_create", "cw_destroy", "cw_last_error", "cw_set_forced_velocity",
     "cw_push", "cw_push_device", "cw_device_outputs", "cw_next_frame_slot", "cw_push_inplace",
     "cw_frames_seen", "cw_read_view", "cw_launch_info", "cw_set_timing",
-    "cw_kernel_time", "cw_copy_to_host", "cw_submit", "cw_wait", "cw_set_detection", "cw_detections",
+    "cw_kernel_time", "cw_copy_to_host", "cw_submit", "cw_submit_raw", "cw_wait", "cw_set_detection", "cw_detections",
     "cw_set_backend", "cw_snapshot_size", "cw_snapshot", "cw_restore",
 )
+
+
+FMT_F32LE, FMT_PGM16 = 0, 1  # cw_submit_raw sample formats (include/cw_b200.h)
 
 
 class NativeUnavailable(RuntimeError):
@@ -101,6 +104,8 @@ def load():
         "cw_copy_to_host": (ctypes.c_int, [vp, vp, vp, ctypes.c_size_t]),
         "cw_submit": (ctypes.c_int, [vp, P(ctypes.c_float), P(ctypes.c_float), P(ctypes.c_float),
                                      P(ctypes.c_uint8), P(i64)]),
+        "cw_submit_raw": (ctypes.c_int, [vp, vp, i32, ctypes.c_double, ctypes.c_double, P(ctypes.c_float),
+                                         P(ctypes.c_float), P(ctypes.c_uint8), P(i64)]),
         "cw_wait": (ctypes.c_int, [vp, i64, P(i32), P(i64)]),
         "cw_set_detection": (ctypes.c_int, [vp, ctypes.c_float, i32]),
         "cw_set_backend": (ctypes.c_int, [vp, i32]),

@@ -111,7 +111,9 @@ struct cw_handle {
     LaunchFn fn;
     Tables tab;
     int grid;
+    int sms = 0;
     cudaStream_t own = nullptr;
+    void *d_raw = nullptr;  // PGM16 upload staging (cw_submit_raw), allocated on first use
     float *d_state = nullptr, *d_that = nullptr, *d_coef = nullptr, *d_frames = nullptr;
     float *d_res = nullptr, *d_pred = nullptr;  // 2 output sets each
     uint8_t *d_vidx = nullptr;
@@ -456,6 +458,7 @@ int cw_create(const cw_params *p, int32_t width, int32_t height, int32_t device,
         return cleanup_fail(CW_ERR_CUDA, "frame kernel cannot be resident on this device");
     const long long units = (long long)h->NXB * (height - halo_rows);
     h->grid = (int)std::min<long long>((long long)occ * sms, std::max<long long>(1, units / 2));
+    h->sms = sms;
 
     const size_t pix_packets = (size_t)height * h->NXB;
     h->state_floats = pix_packets * fn.nsp * 32 * 2;
@@ -500,6 +503,7 @@ void cw_destroy(cw_handle *h)
     cudaFree(h->d_that);
     cudaFree(h->d_coef);
     cudaFree(h->d_frames);
+    cudaFree(h->d_raw);
     cudaFree(h->d_res);
     cudaFree(h->d_pred);
     cudaFree(h->d_vidx);
@@ -722,10 +726,57 @@ int cw_device_outputs(cw_handle *h, float **residual, float **prediction, uint8_
 //  of that slot (as the delayed frame of n-2 ... or current frame n-R);
 //  kernel(n) waits for H2D(n) and for D2H(n-2), which read output set n % 2;
 //  D2H(n) waits for kernel(n).  Host buffers should be pinned.
+// PGM16 payload -> float32 frame slot: big-endian u16 q, v = f32(f64(q) *
+// scale + offset) with the multiply and add rounded separately, as numpy
+// evaluates q.astype(f64) * scale + offset (seqio.py:199-202).  8 samples
+// per thread from one 16-byte load.
+__global__ void cw_decode_pgm16_kernel(const uint16_t *__restrict__ src, float *__restrict__ dst, size_t n,
+                                       double scale, double offset)
+{
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    const size_t n8 = n / 8;
+    auto cvt = [&](uint32_t q) { return (float)__dadd_rn(__dmul_rn((double)q, scale), offset); };
+    for (size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x; k < n8; k += stride) {
+        const uint4 v = reinterpret_cast<const uint4 *>(src)[k];
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+        float *o = dst + 8 * k;
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const uint32_t s = __byte_perm(w[j], 0, 0x2301);  // swap the bytes of both halves
+            o[2 * j] = cvt(s & 0xffffu);
+            o[2 * j + 1] = cvt(s >> 16);
+        }
+    }
+    for (size_t i = 8 * n8 + (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const uint32_t q = src[i];
+        dst[i] = cvt(((q & 0xffu) << 8) | (q >> 8));
+    }
+}
+
+static int submit_impl(cw_handle *h, const void *samples, int format, double scale, double offset,
+                       float *residual, float *prediction, uint8_t *vidx, int64_t *ticket);
+
 int cw_submit(cw_handle *h, const float *frame, float *residual, float *prediction, uint8_t *vidx,
               int64_t *ticket)
 {
+    return submit_impl(h, frame, CW_FMT_F32LE, 1.0, 0.0, residual, prediction, vidx, ticket);
+}
+
+int cw_submit_raw(cw_handle *h, const void *samples, int32_t format, double scale, double offset,
+                  float *residual, float *prediction, uint8_t *vidx, int64_t *ticket)
+{
+    if (h && format != CW_FMT_F32LE && format != CW_FMT_PGM16)
+        return fail(h, CW_ERR_VALUE, "unknown sample format");
+    if (h && format == CW_FMT_PGM16 && !(scale > 0.0))
+        return fail(h, CW_ERR_VALUE, "scale must be > 0");
+    return submit_impl(h, samples, format, scale, offset, residual, prediction, vidx, ticket);
+}
+
+static int submit_impl(cw_handle *h, const void *samples, int format, double scale, double offset,
+                       float *residual, float *prediction, uint8_t *vidx, int64_t *ticket)
+{
     NvtxRange nvtx("cw_submit");
+    const void *frame = samples;
     if (!h || !frame || !ticket)
         return CW_ERR_VALUE;
     const size_t HW = (size_t)h->W * h->H;
@@ -736,7 +787,19 @@ int cw_submit(cw_handle *h, const float *frame, float *residual, float *predicti
     if (n >= 2)
         CW_CUDA(h, cudaStreamWaitEvent(h->up, h->ev_k[(n - 2) % cw_handle::NEV], 0));
     float *slot = h->d_frames + (size_t)(n % h->nslots) * HW;
-    CW_CUDA(h, cudaMemcpyAsync(slot, frame, HW * 4, cudaMemcpyHostToDevice, h->up));
+    if (format == CW_FMT_PGM16) {
+        if (!h->d_raw) {
+            CW_CUDA(h, cudaMalloc(&h->d_raw, HW * 2 + 16));
+        }
+        // the staging buffer is reused in `up` stream order: H2D(n+1) follows decode(n)
+        CW_CUDA(h, cudaMemcpyAsync(h->d_raw, frame, HW * 2, cudaMemcpyHostToDevice, h->up));
+        const int blocks = (int)std::min<size_t>((HW / 8 + 255) / 256 + 1, (size_t)h->sms * 8);
+        cw_decode_pgm16_kernel<<<blocks, 256, 0, h->up>>>(reinterpret_cast<const uint16_t *>(h->d_raw), slot, HW,
+                                                         scale, offset);
+        CW_CUDA(h, cudaGetLastError());
+    } else {
+        CW_CUDA(h, cudaMemcpyAsync(slot, frame, HW * 4, cudaMemcpyHostToDevice, h->up));
+    }
     CW_CUDA(h, cudaEventRecord(h->ev_up[e], h->up));
     CW_CUDA(h, cudaStreamWaitEvent(h->own, h->ev_up[e], 0));
     if (n >= 2)

@@ -113,7 +113,7 @@ __device__ __forceinline__ void detect_epilogue(const FrameArgs &a, bool valid, 
     unsigned long long key =
         valid ? ((unsigned long long)__float_as_uint(v) << 32) | (0xffffffffull - (unsigned long long)((size_t)oy * a.W + ox))
               : 0ull;
-    float sq = valid ? res * res : 0.f;
+    double sq = valid ? (double)res * (double)res : 0.0;  // exact square, as f64(res)**2
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         const unsigned long long k2 = __shfl_xor_sync(0xffffffffu, key, o);
@@ -123,7 +123,7 @@ __device__ __forceinline__ void detect_epilogue(const FrameArgs &a, bool valid, 
     const unsigned int nv = __popc(__ballot_sync(0xffffffffu, valid));
     if ((threadIdx.x & 31) == 0 && nv) {
         atomicMax(peak, key);
-        atomicAdd(sumsq, (double)sq);
+        atomicAdd(sumsq, sq);
         atomicAdd(nval, (unsigned long long)nv);
     }
 }

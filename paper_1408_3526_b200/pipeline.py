@@ -282,7 +282,8 @@ class Pipeline:
             return None
         return self._wrap(int(fidx.value), res, pred, vidx, ticket=self.frames_seen - 1)
 
-    def process_stream(self, frames, depth: int = 3):
+    def process_stream(self, frames, depth: int = 3, sample_format: str = "f32le",
+                       scale: float = 1.0, offset: float = 0.0):
         """Pipelined ``process_frame`` over an iterable of (H, W) frames.
 
         Yields the same WhitenedOutput sequence as calling ``process_frame``
@@ -291,12 +292,23 @@ class Pipeline:
         download of frame n-1 overlap the kernel of frame n (cw_submit /
         cw_wait).  Pinned input frames (e.g. numpy views
         of ``torch.empty(..., pin_memory=True)``) give fully async uploads.
+
+        ``sample_format="pgm16"`` takes frames as the raw big-endian uint16
+        samples of a PGM16 sequence (dtype ">u2", e.g. from
+        ``seqio.SequenceReader.read_raw``): they are uploaded as 16-bit words
+        and de-quantised on the GPU as f32(f64(q) * scale + offset), the
+        value ``seqio.read_sequence`` returns.
         """
         from collections import deque
 
         lib = _native.load()
         depth = max(1, min(int(depth), 6))
         h, w = self.height, self.width
+        if sample_format not in ("f32le", "pgm16"):
+            raise ValueError(f"unknown sample format {sample_format!r}")
+        pgm = sample_format == "pgm16"
+        if pgm and not scale > 0:
+            raise ValueError("scale must be > 0")
         inflight: deque = deque()
 
         def collect(item):
@@ -306,15 +318,17 @@ class Pipeline:
             return self._wrap(int(fidx.value), res, pred, vidx, ticket=ticket) if ready.value else None
 
         for frame in frames:
-            frame = np.ascontiguousarray(frame, dtype=np.float32)
+            frame = np.ascontiguousarray(frame, dtype=">u2" if pgm else np.float32)
             if frame.shape != (h, w):
                 raise ValueError(f"frame shape {frame.shape} != {(h, w)}")
             res = self._pool.take((h, w), np.float32)
             pred = self._pool.take((h, w), np.float32)
             vidx = self._pool.take((h, w, 2), np.uint8)
             ticket = ctypes.c_int64(-1)
-            rc = lib.cw_submit(self._h, _native.fptr(frame), _native.fptr(res), _native.fptr(pred),
-                               vidx.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), ctypes.byref(ticket))
+            rc = lib.cw_submit_raw(self._h, ctypes.c_void_p(frame.ctypes.data),
+                                   _native.FMT_PGM16 if pgm else _native.FMT_F32LE, float(scale), float(offset),
+                                   _native.fptr(res), _native.fptr(pred),
+                                   vidx.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), ctypes.byref(ticket))
             _native.check(rc, self._h)
             inflight.append((ticket.value, frame, res, pred, vidx))
             while len(inflight) > depth:

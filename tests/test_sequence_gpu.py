@@ -1,0 +1,205 @@
+"""Sequence ingest / egress on the GPU (§8f rank 1): ``filter_sequence``
+and the raw-sample upload path ``cw_submit_raw``.
+
+The product path here is the same fused kernel as ``process_frame``, so
+its outputs must be BIT-identical to ``process_frame`` on the frames that
+``read_sequence`` returns; the PGM16 device decode must reproduce the
+reference reader's float32 values bit for bit (fixtures written by the
+reference, tests/golden/seq).
+"""
+
+import ctypes
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _ref_outputs(params, frames):
+    from paper_1408_3526_b200 import Pipeline
+
+    res, pred, idx, fidx = [], [], [], []
+    with Pipeline(params, frames.shape[2], frames.shape[1]) as pipe:
+        for f in frames:
+            o = pipe.process_frame(f)
+            if o is not None:
+                res.append(o.residual)
+                pred.append(o.prediction)
+                idx.append(o.velocity.indices)
+                fidx.append(o.frame_index)
+    return np.stack(res), np.stack(pred), np.stack(idx), fidx
+
+
+def test_pgm16_device_decode_is_bit_exact():
+    """cw_submit_raw(PGM16): the frame written into the ring slot equals
+    the reference reader's f32(f64(q) * scale + offset) for every sample."""
+    from paper_1408_3526_b200 import Pipeline, _native, default_params
+    from paper_1408_3526_b200.seqio import SequenceReader
+
+    exp = np.load(os.path.join(GOLD, "seq_expected.npz"))
+    rng = np.random.default_rng(5)
+    lib = _native.load()
+    # reference-written fixture (9 x 11: the sample count is not a multiple
+    # of the kernel's 8-sample vector) + synthetic frames; the 6 x 8 fixture
+    # is smaller than the analysis window, so no pipeline can take it
+    for name in ("pgm16_signed", "all_codes", "odd_fixed_scale"):
+        if name != "pgm16_signed":
+            if name == "all_codes":  # every 16-bit code once, awkward scale/offset
+                q = rng.permutation(np.arange(65536, dtype=np.uint32)).astype(">u2").reshape(256, 256)
+                scale, offset = 3.0e-5 * np.pi, -1.0 / 3.0
+            else:
+                q = rng.integers(0, 65536, size=(13, 29)).astype(">u2")
+                scale, offset = 1.0 / 512, 4.0
+            frames_q = [q]
+            want = [(q.astype(np.float64) * scale + offset).astype(np.float32)]
+        else:
+            rd = SequenceReader(os.path.join(GOLD, "seq", name))
+            frames_q = []
+            for t in range(len(rd)):
+                raw = np.empty(rd.shape, ">u2")
+                rd.read_raw(t, raw)
+                frames_q.append(raw)
+            scale, offset = rd.header.scale, rd.header.offset
+            want = list(exp[f"{name}__read"])
+        h, w = frames_q[0].shape
+        with Pipeline(default_params(), w, h) as pipe:
+            for q, ref in zip(frames_q, want):
+                slot = ctypes.c_void_p()
+                _native.check(lib.cw_next_frame_slot(pipe._h, ctypes.byref(slot)), pipe._h)
+                res = np.empty((h, w), np.float32)
+                vidx = np.empty((h, w, 2), np.uint8)
+                tk = ctypes.c_int64(-1)
+                _native.check(lib.cw_submit_raw(pipe._h, ctypes.c_void_p(q.ctypes.data), _native.FMT_PGM16, scale,
+                                                offset, _native.fptr(res), None,
+                                                vidx.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)),
+                                                ctypes.byref(tk)), pipe._h)
+                rdy, fi = ctypes.c_int32(), ctypes.c_int64()
+                _native.check(lib.cw_wait(pipe._h, tk, ctypes.byref(rdy), ctypes.byref(fi)), pipe._h)
+                got = np.empty((h, w), np.float32)
+                _native.check(lib.cw_copy_to_host(pipe._h, got.ctypes.data, slot, got.nbytes), pipe._h)
+                assert np.array_equal(got.view(np.uint32), ref.view(np.uint32)), name
+
+
+def test_submit_raw_rejects_bad_format():
+    from paper_1408_3526_b200 import Pipeline, _native, default_params
+
+    lib = _native.load()
+    buf = np.zeros((16, 16), np.float32)
+    with Pipeline(default_params(), 16, 16) as pipe:
+        tk = ctypes.c_int64()
+        rc = lib.cw_submit_raw(pipe._h, ctypes.c_void_p(buf.ctypes.data), 7, 1.0, 0.0, None, None, None,
+                               ctypes.byref(tk))
+        assert rc == -2
+        rc = lib.cw_submit_raw(pipe._h, ctypes.c_void_p(buf.ctypes.data), _native.FMT_PGM16, 0.0, 0.0, None, None,
+                               None, ctypes.byref(tk))
+        assert rc == -2
+
+
+@pytest.mark.parametrize("dtype_in", ["f32le", "pgm16"])
+def test_filter_sequence_matches_process_frame(params, tmp_path, dtype_in):
+    from paper_1408_3526_b200.seqio import read_sequence, write_sequence
+    from paper_1408_3526_b200.sequence import METRICS_HEADER, filter_sequence, metrics_row
+
+    frames = golden("c1_64x64x32.npz")["frames"][:20]
+    write_sequence(frames, tmp_path / "in", dtype=dtype_in, meta={"seed": 0})
+    decoded, _ = read_sequence(tmp_path / "in")  # pgm16: the quantised frames
+    res, pred, idx, fidx = _ref_outputs(params, decoded)
+
+    out = tmp_path / "out"
+    meta = filter_sequence(tmp_path / "in", out, params, emit_prediction=True, emit_velocity=True,
+                           metrics=tmp_path / "m.csv", depth=3)
+    got_res, hdr = read_sequence(out)
+    assert np.array_equal(got_res, res)
+    assert hdr.meta["first_frame_index"] == fidx[0] == params.latency
+    assert hdr.meta["latency_frames"] == params.latency
+    got_pred, phdr = read_sequence(out / "prediction")
+    assert np.array_equal(got_pred, pred) and phdr.meta["source"] == "filter-prediction"
+    vel = np.fromfile(out / "velocity.f32", dtype="<f4").reshape(len(fidx), 64, 64, 2)
+    lag = np.asarray(params.lag_grid_x, np.float64)
+    want_vel = np.stack([lag[idx[..., 0]], lag[idx[..., 1]]], -1).astype(np.float32)
+    assert np.array_equal(vel, want_vel)
+    side = json.loads((out / "velocity.json").read_text())
+    assert side["frame_count"] == len(fidx) and side["first_frame_index"] == fidx[0]
+
+    # metrics rows from the fused epilogue == host rows from the same outputs
+    lines = (tmp_path / "m.csv").read_text().strip().split("\n")
+    assert lines[0] == METRICS_HEADER and len(lines) == 1 + len(fidx)
+
+    class O:
+        pass
+
+    from paper_1408_3526_b200.pipeline import valid_mask
+
+    mask = valid_mask(params, 64, 64)
+    for k, line in enumerate(lines[1:]):
+        o = O()
+        o.frame_index, o.residual, o.mask, o.metrics, o.velocity = fidx[k], res[k], mask, None, None
+        assert line == metrics_row(o, params, None).csv()
+
+    assert meta["frames_in"] == 20 and meta["frames_out"] == len(fidx)
+    assert meta["valid_region"] == {"x": [4, 59], "y": [4, 59]}
+    assert json.loads((out / "run_meta.json").read_text())["frames_out"] == len(fidx)
+
+
+def test_filter_sequence_ground_truth_metrics(params, tmp_path):
+    """With ground_truth.json the rows carry target / hit / velocity errors
+    computed as cli.compute_metrics_row from the filtered outputs."""
+    from paper_1408_3526_b200.scenegen import SimConfig, generate, target_center
+    from paper_1408_3526_b200.seqio import write_sequence
+    from paper_1408_3526_b200.sequence import filter_sequence, load_ground_truth, metrics_row
+    from paper_1408_3526_b200.pipeline import valid_mask
+
+    cfg = SimConfig(width=48, height=40, frame_count=14, rng_seed=3)
+    frames, comps = generate(cfg)
+    write_sequence(frames, tmp_path / "in", meta={"seed": 3})
+    truth = {"config": {"psf_sigma": cfg.psf_sigma, "target_peak": cfg.target_peak,
+                        "target_truncation": cfg.target_truncation},
+             "seed": 3, "components": comps.tolist(), "clutter_velocity": list(cfg.clutter_velocity),
+             "target_centers": [list(target_center(cfg, t)) for t in range(cfg.frame_count)]}
+    (tmp_path / "in" / "ground_truth.json").write_text(json.dumps(truth))
+    filter_sequence(tmp_path / "in", tmp_path / "out", params, metrics=tmp_path / "m.csv")
+    res, _, idx, fidx = _ref_outputs(params, frames)
+    gt = load_ground_truth(tmp_path / "in")
+    lag = np.asarray(params.lag_grid_x, np.float64)
+    mask = valid_mask(params, 48, 40)
+    lines = (tmp_path / "m.csv").read_text().strip().split("\n")[1:]
+    assert len(lines) == len(fidx)
+    for k, line in enumerate(lines):
+        class O:
+            pass
+        o = O()
+        o.frame_index, o.residual, o.mask, o.metrics = fidx[k], res[k], mask, None
+
+        class V:
+            velocities = np.stack([lag[idx[k][..., 0]], lag[idx[k][..., 1]]], -1).astype(np.float32).astype(np.float64)
+        o.velocity = V
+        assert line == metrics_row(o, params, gt).csv()
+        assert line.split(",")[7] in ("0", "1")
+
+
+def test_process_stream_pgm16_matches_decoded_frames(params, tmp_path):
+    from paper_1408_3526_b200 import Pipeline
+    from paper_1408_3526_b200.seqio import SequenceReader, read_sequence, write_sequence
+
+    frames = golden("c1_64x64x32.npz")["frames"][:12]
+    write_sequence(frames, tmp_path / "s", dtype="pgm16")
+    decoded, hdr = read_sequence(tmp_path / "s")
+    res, pred, idx, fidx = _ref_outputs(params, decoded)
+    rd = SequenceReader(tmp_path / "s")
+    raws = []
+    for t in range(len(rd)):
+        q = np.empty(rd.shape, ">u2")
+        rd.read_raw(t, q)
+        raws.append(q)
+    with Pipeline(params, 64, 64) as pipe:
+        outs = list(pipe.process_stream(raws, depth=3, sample_format="pgm16", scale=hdr.scale, offset=hdr.offset))
+    assert [o.frame_index for o in outs] == fidx
+    for k, o in enumerate(outs):
+        assert np.array_equal(o.residual, res[k]) and np.array_equal(o.velocity.indices, idx[k])
