@@ -583,7 +583,6 @@ static int run_frame(cw_handle *h, cudaStream_t s, int32_t *ready, int64_t *fram
     a.res = h->d_res + set * HW;
     a.pred = h->d_pred + set * HW;
     a.vidx = h->d_vidx + set * HW * 2;
-    a.vidx_prev = (n >= 1) ? h->d_vidx + (set ^ 1) * HW * 2 : nullptr;
     a.W = h->W;
     a.H = h->H;
     a.NXB = h->NXB;

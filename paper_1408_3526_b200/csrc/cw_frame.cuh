@@ -80,7 +80,6 @@ struct FrameArgs {
     float *res;            // (H, W) residual out
     float *pred;           // (H, W) prediction out (nullable)
     uint8_t *vidx;         // (H, W, 2) velocity index out
-    const uint8_t *vidx_prev;  // previous frame's velocities (PEF coefficient prefetch guess)
     int W, H, NXB;
     int y_begin;           // first local anchor row (strip halo)
     int y_off;             // global row of local row 0
