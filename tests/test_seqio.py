@@ -202,3 +202,14 @@ def test_metrics_row_from_fused_stats():
               "n_valid": int(mask.sum())}
         row = metrics_row(_O(2 + k, r, mask, None, st), p, None)
         assert row.csv() == str(EXP["metrics__rows_no_truth"][k])
+
+
+def test_writer_reproduces_reference_cli_input(tmp_path):
+    """The input sequence of the reference CLI golden run (make_cli_golden.py)
+    re-written by our writer: identical header and payload bytes."""
+    g = np.load(os.path.join(GOLD, "cli_filter.npz"))
+    hdr = g["input_header"].tobytes().decode()
+    write_sequence(g["frames"], tmp_path / "s", meta=json.loads(hdr)["meta"])
+    assert (tmp_path / "s" / "header.json").read_text() == hdr
+    back, _ = read_sequence(tmp_path / "s")
+    assert np.array_equal(back, g["frames"])

@@ -203,3 +203,62 @@ def test_process_stream_pgm16_matches_decoded_frames(params, tmp_path):
     assert [o.frame_index for o in outs] == fidx
     for k, o in enumerate(outs):
         assert np.array_equal(o.residual, res[k]) and np.array_equal(o.velocity.indices, idx[k])
+
+
+def test_filter_sequence_vs_reference_cli(params, tmp_path):
+    """The reference's own `clutterwhiten simulate` + `filter --metrics
+    --emit-prediction --emit-velocity` run (tests/golden/make_cli_golden.py)
+    replayed through filter_sequence: same files, same metadata, outputs
+    within the stated parity tolerances (tests/parity.py)."""
+    from parity import RES_TOL, VEL_FRAC, agreeing_outputs, anchor_mask
+
+    from paper_1408_3526_b200.pipeline import valid_mask
+    from paper_1408_3526_b200.seqio import read_sequence, write_sequence
+    from paper_1408_3526_b200.sequence import METRICS_HEADER, filter_sequence
+
+    g = golden("cli_filter.npz")
+    txt = lambda k: g[k].tobytes().decode()
+    frames = g["frames"]
+    write_sequence(frames, tmp_path / "seq", meta=json.loads(txt("input_header"))["meta"])
+    assert (tmp_path / "seq" / "header.json").read_text() == txt("input_header")
+    (tmp_path / "seq" / "ground_truth.json").write_text(txt("ground_truth"))
+    out = tmp_path / "res"
+    meta = filter_sequence(tmp_path / "seq", out, params, emit_prediction=True, emit_velocity=True,
+                           metrics=tmp_path / "m.csv")
+
+    res, hres = read_sequence(out)
+    pred, hpred = read_sequence(out / "prediction")
+    ref_h, ref_ph = json.loads(txt("residual_header")), json.loads(txt("prediction_header"))
+    for mine, ref in ((hres, ref_h), (hpred, ref_ph)):
+        d = mine.to_json_dict()
+        d["meta"].pop("input")
+        ref["meta"].pop("input")
+        assert d == ref
+    assert json.loads((out / "velocity.json").read_text()) == json.loads(txt("velocity_json"))
+    ref_meta = json.loads(txt("run_meta"))
+    for k in ("command", "params", "strategy", "backend", "input_seed", "frames_in", "frames_out",
+              "valid_region", "latency_frames"):
+        assert meta[k] == ref_meta[k], k
+
+    t, h, w = g["residual"].shape
+    vel = np.fromfile(out / "velocity.f32", dtype="<f4").reshape(t, h, w, 2)
+    vel_ref = g["velocity"].reshape(t, h, w, 2)
+    amask = anchor_mask(params, h, w)
+    fmax = float(np.abs(frames).max())
+    vmask = valid_mask(params, w, h)
+    for k in range(t):
+        same = np.all(vel[k] == vel_ref[k], axis=-1)
+        assert same[amask].mean() >= VEL_FRAC
+        ok = agreeing_outputs(vel[k], vel_ref[k], params) & vmask
+        assert np.abs(res[k][ok].astype(np.float64) - g["residual"][k][ok]).max() <= RES_TOL * fmax
+        assert np.abs(pred[k][ok].astype(np.float64) - g["prediction"][k][ok]).max() <= RES_TOL * fmax
+        assert np.all(res[k][~vmask] == 0)
+
+    lines = (tmp_path / "m.csv").read_text().strip().split("\n")
+    ref_lines = txt("metrics").strip().split("\n")
+    assert lines[0] == ref_lines[0] == METRICS_HEADER and len(lines) == len(ref_lines)
+    for a, b in zip(lines[1:], ref_lines[1:]):
+        fa, fb = a.split(","), b.split(",")
+        assert fa[0] == fb[0] and fa[3:8] == fb[3:8]  # frame, peak x/y, target x/y, hit
+        for i in (1, 2, 8, 9):  # rms, peak value, velocity-error stats (tolerance in the last digit)
+            assert abs(float(fa[i]) - float(fb[i])) <= 1e-4 * max(1.0, abs(float(fb[i]))), (i, a, b)
