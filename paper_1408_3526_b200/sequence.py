@@ -47,7 +47,7 @@ from .pipeline import Pipeline, valid_bounds
 from .seqio import SequenceError, SequenceReader, SequenceWriter
 
 __all__ = ["METRICS_HEADER", "MetricsRow", "GroundTruthLite", "load_ground_truth", "target_exclusion_radius",
-           "metrics_row", "filter_sequence"]
+           "metrics_row", "filter_sequence", "flow_sequence"]
 
 GROUND_TRUTH_NAME = "ground_truth.json"
 RUN_META_NAME = "run_meta.json"
@@ -165,35 +165,18 @@ def _pinned(nbytes: int) -> np.ndarray:
     return torch.empty(nbytes, dtype=torch.uint8, pin_memory=True).numpy()
 
 
-def filter_sequence(input_dir, out_dir, params: FilterParams | None = None, *, dtype: str = "f32le",
-                    emit_prediction: bool = False, emit_velocity: bool = False, metrics=None,
-                    spectrum_backend: str = "recursive", depth: int = 3, device: int = 0) -> dict:
-    """Whiten the sequence in ``input_dir`` into ``out_dir`` (cli._cmd_filter
-    semantics, cli.py:230-306); returns the run-meta dict it also writes."""
-    params = default_params() if params is None else params
-    out_dir = Path(out_dir)
-    reader = SequenceReader(input_dir)
-    truth = load_ground_truth(input_dir)
-    h, w = reader.shape
-    t_total = len(reader)
-    depth = max(1, min(int(depth), 6))
-    pgm = reader.pgm
-    hdr = reader.header
-    want_metrics = metrics is not None
-
-    pipe = Pipeline(params, w, h, spectrum_backend=spectrum_backend, device=device,
-                    detect_threshold=0.0 if want_metrics else None, max_detections=0)
+def _stream(reader: SequenceReader, pipe: Pipeline, consume, *, want_pred: bool, want_stats: bool,
+            depth: int) -> float:
+    """Run every frame of ``reader`` through ``pipe``: a reader thread fills
+    pinned payload buffers, the calling thread keeps ``depth`` frames in
+    flight through cw_submit_raw / cw_wait, and a writer thread calls
+    ``consume(frame_index, input_index, residual, prediction, vidx, stats)``
+    for each ready output in order (its arrays are recycled afterwards).
+    Returns the wall-clock seconds of the run."""
     lib = _native.load()
-    out_dir.mkdir(parents=True, exist_ok=True)
-    seq_meta = {"source": "filter", "input": str(input_dir), "first_frame_index": None,
-                "latency_frames": params.latency}
-    res_w = SequenceWriter(out_dir, w, h, dtype=dtype)
-    pred_w = SequenceWriter(out_dir / "prediction", w, h, dtype=dtype) if emit_prediction else None
-    vel_fh = open(out_dir / "velocity.f32", "wb") if emit_velocity else None
-    lut_v = pipe._lut_v.astype("<f4")  # (ix | iy << 8) -> (vx, vy), f64 lags rounded to f32
-    rows: list[MetricsRow] = []
-
-    # staging: input payloads and output sets, recycled through free lists
+    h, w = reader.shape
+    hdr = reader.header
+    depth = max(1, min(int(depth), 6))
     n_in, n_out = depth + 3, depth + 4
     free_in: queue.Queue = queue.Queue()
     for _ in range(n_in):
@@ -206,18 +189,16 @@ def filter_sequence(input_dir, out_dir, params: FilterParams | None = None, *, d
     ready_in: queue.Queue = queue.Queue(maxsize=n_in)
     to_write: queue.Queue = queue.Queue(maxsize=n_out)
     errors: list[BaseException] = []
-    first_index = [None]
-    frames_out = [0]
 
     def read_loop():
         try:
-            for t in range(t_total):
+            for t in range(len(reader)):
                 buf = free_in.get()
                 if buf is None:
                     return
                 reader.read_raw(t, buf)
                 ready_in.put((t, buf))
-        except BaseException as exc:  # surfaced on the main thread
+        except BaseException as exc:  # surfaced on the calling thread
             errors.append(exc)
         ready_in.put(None)
 
@@ -227,8 +208,88 @@ def filter_sequence(input_dir, out_dir, params: FilterParams | None = None, *, d
                 item = to_write.get()
                 if item is None:
                     return
-                fidx, outs, stats = item
-                res, pred, vidx = outs
+                fidx, t_in, outs, stats = item
+                consume(fidx, t_in, outs[0], outs[1], outs[2], stats)
+                free_out.put(outs)
+        except BaseException as exc:
+            errors.append(exc)
+
+    inflight = []
+
+    def collect():
+        ticket, buf, outs = inflight.pop(0)
+        ready, fidx = ctypes.c_int32(0), ctypes.c_int64(-1)
+        _native.check(lib.cw_wait(pipe._h, ticket, ctypes.byref(ready), ctypes.byref(fidx)), pipe._h)
+        free_in.put(buf)
+        if not ready.value:
+            free_out.put(outs)
+            return
+        stats = None
+        if want_stats:
+            st = np.zeros(5, np.float64)
+            n = ctypes.c_int32(0)
+            _native.check(lib.cw_detections(pipe._h, ticket, ctypes.byref(n), None, 0,
+                                            st.ctypes.data_as(ctypes.POINTER(ctypes.c_double))), pipe._h)
+            stats = {"peak_abs_residual": float(st[0]), "peak_x": int(st[1]), "peak_y": int(st[2]),
+                     "sum_sq": float(st[3]), "n_valid": int(st[4])}
+        to_write.put((int(fidx.value), ticket, outs, stats))
+
+    reader_t = threading.Thread(target=read_loop, name="cw-ingest", daemon=True)
+    writer_t = threading.Thread(target=write_loop, name="cw-egress", daemon=True)
+    fmt = _native.FMT_PGM16 if reader.pgm else _native.FMT_F32LE
+    t0 = time.perf_counter()
+    reader_t.start()
+    writer_t.start()
+    try:
+        while not errors:
+            item = ready_in.get()
+            if item is None:
+                break
+            _, buf = item
+            res, pred, vidx = free_out.get()
+            ticket = ctypes.c_int64(-1)
+            _native.check(lib.cw_submit_raw(
+                pipe._h, ctypes.c_void_p(buf.ctypes.data), fmt, float(hdr.scale), float(hdr.offset),
+                _native.fptr(res), _native.fptr(pred) if want_pred else None,
+                vidx.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), ctypes.byref(ticket)), pipe._h)
+            inflight.append((ticket.value, buf, (res, pred, vidx)))
+            while len(inflight) > depth:
+                collect()
+        while inflight:
+            collect()
+    finally:
+        free_in.put(None)  # unblock the reader if it waits for a buffer
+        to_write.put(None)
+        writer_t.join()
+        reader_t.join(timeout=5.0)
+    if errors:
+        raise errors[0]
+    return time.perf_counter() - t0
+
+
+def filter_sequence(input_dir, out_dir, params: FilterParams | None = None, *, dtype: str = "f32le",
+                    emit_prediction: bool = False, emit_velocity: bool = False, metrics=None,
+                    spectrum_backend: str = "recursive", depth: int = 3, device: int = 0) -> dict:
+    """Whiten the sequence in ``input_dir`` into ``out_dir`` (cli._cmd_filter
+    semantics, cli.py:230-306); returns the run-meta dict it also writes."""
+    params = default_params() if params is None else params
+    out_dir = Path(out_dir)
+    truth = load_ground_truth(input_dir)
+    want_metrics = metrics is not None
+    with SequenceReader(input_dir) as reader:
+        h, w = reader.shape
+        hdr = reader.header
+        out_dir.mkdir(parents=True, exist_ok=True)
+        res_w = SequenceWriter(out_dir, w, h, dtype=dtype)
+        pred_w = SequenceWriter(out_dir / "prediction", w, h, dtype=dtype) if emit_prediction else None
+        vel_fh = open(out_dir / "velocity.f32", "wb") if emit_velocity else None
+        rows: list[MetricsRow] = []
+        first_index = [None]
+        with Pipeline(params, w, h, spectrum_backend=spectrum_backend, device=device,
+                      detect_threshold=0.0 if want_metrics else None, max_detections=0) as pipe:
+            lut_v = pipe._lut_v.astype("<f4")  # (ix | iy << 8) -> (vx, vy), f64 lags rounded to f32
+
+            def consume(fidx, _t, res, pred, vidx, stats):
                 if first_index[0] is None:
                     first_index[0] = fidx
                 res_w.append(res)
@@ -242,97 +303,104 @@ def filter_sequence(input_dir, out_dir, params: FilterParams | None = None, *, d
                 if want_metrics:
                     velocity = None if vel is None else SimpleNamespace(velocities=vel.astype(np.float64))
                     rows.append(metrics_row(_Out(fidx, res, pipe.mask, velocity, stats), params, truth))
-                frames_out[0] += 1
-                free_out.put(outs)
-        except BaseException as exc:
-            errors.append(exc)
 
-    reader_t = threading.Thread(target=read_loop, name="cw-ingest", daemon=True)
-    writer_t = threading.Thread(target=write_loop, name="cw-egress", daemon=True)
-    t0 = time.perf_counter()
-    reader_t.start()
-    writer_t.start()
-    inflight = []
-
-    def collect():
-        ticket, buf, outs = inflight.pop(0)
-        ready, fidx = ctypes.c_int32(0), ctypes.c_int64(-1)
-        _native.check(lib.cw_wait(pipe._h, ticket, ctypes.byref(ready), ctypes.byref(fidx)), pipe._h)
-        free_in.put(buf)
-        if not ready.value:
-            free_out.put(outs)
-            return
-        stats = None
-        if want_metrics:
-            st = np.zeros(5, np.float64)
-            n = ctypes.c_int32(0)
-            _native.check(lib.cw_detections(pipe._h, ticket, ctypes.byref(n), None, 0,
-                                            st.ctypes.data_as(ctypes.POINTER(ctypes.c_double))), pipe._h)
-            stats = {"peak_abs_residual": float(st[0]), "peak_x": int(st[1]), "peak_y": int(st[2]),
-                     "sum_sq": float(st[3]), "n_valid": int(st[4])}
-        to_write.put((int(fidx.value), outs, stats))
-
-    try:
-        with pipe:
-            fmt = _native.FMT_PGM16 if pgm else _native.FMT_F32LE
-            while True:
-                item = ready_in.get()
-                if item is None:
-                    break
-                _, buf = item
-                res, pred, vidx = free_out.get()
-                ticket = ctypes.c_int64(-1)
-                _native.check(lib.cw_submit_raw(
-                    pipe._h, ctypes.c_void_p(buf.ctypes.data), fmt, float(hdr.scale), float(hdr.offset),
-                    _native.fptr(res), _native.fptr(pred) if pred_w is not None else None,
-                    vidx.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), ctypes.byref(ticket)), pipe._h)
-                inflight.append((ticket.value, buf, (res, pred, vidx)))
-                while len(inflight) > depth:
-                    collect()
-            while inflight:
-                collect()
+            try:
+                elapsed = _stream(reader, pipe, consume, want_pred=pred_w is not None, want_stats=want_metrics,
+                                  depth=depth)
+            finally:
+                if vel_fh is not None:
+                    vel_fh.close()
             bank_seconds = pipe.bank.build_seconds
-    finally:
-        free_in.put(None)  # unblock the reader if it is waiting for a buffer
-        to_write.put(None)
-        writer_t.join()
-        reader_t.join(timeout=5.0)
-        reader.close()
-        if vel_fh is not None:
-            vel_fh.close()
-    if errors:
-        raise errors[0]
-    elapsed = time.perf_counter() - t0
-    if frames_out[0] == 0:
+    n_out = res_w.count
+    if n_out == 0:
         raise SequenceError("sequence shorter than the temporal window")
-
-    seq_meta["first_frame_index"] = first_index[0]
+    seq_meta = {"source": "filter", "input": str(input_dir), "first_frame_index": first_index[0],
+                "latency_frames": params.latency}
     res_w.meta = dict(seq_meta)
     res_w.close()
     if pred_w is not None:
         pred_w.meta = dict(seq_meta, source="filter-prediction")
         pred_w.close()
     if emit_velocity:
-        with open(out_dir / "velocity.json", "w", encoding="utf-8") as fh:
-            json.dump({"width": w, "height": h, "frame_count": frames_out[0], "channels": 2,
-                       "components": ["vx", "vy"], "dtype": "f32le", "first_frame_index": first_index[0]},
-                      fh, indent=2)
-            fh.write("\n")
+        _velocity_sidecar(out_dir, n_out, w, h, first_index[0])
     if want_metrics:
         with open(metrics, "w", encoding="utf-8") as fh:
             fh.write(METRICS_HEADER + "\n")
             for row in rows:
                 fh.write(row.csv() + "\n")
     ox_lo, ox_hi, oy_lo, oy_hi = valid_bounds(params, w, h)
-    meta = {
+    return _run_meta(out_dir, {
         "command": "filter", "params": params_as_dict(params), "strategy": "serial",
         "backend": spectrum_backend, "input": str(input_dir), "input_seed": hdr.meta.get("seed"),
-        "frames_in": t_total, "frames_out": frames_out[0],
+        "frames_in": len(reader), "frames_out": n_out,
         "valid_region": {"x": [ox_lo, ox_hi], "y": [oy_lo, oy_hi]},
         "latency_frames": params.latency, "bank_build_seconds": bank_seconds, "seconds": elapsed,
-        "version": __version__, "device": "cuda", "sample_format": hdr.dtype,
-    }
-    with open(out_dir / RUN_META_NAME, "w", encoding="utf-8") as fh:
-        json.dump(meta, fh, indent=2, default=float)
+        "device": "cuda", "sample_format": hdr.dtype,
+    })
+
+
+def flow_sequence(input_dir, out_dir, params: FilterParams | None = None, *, fmt: str = "f32",
+                  depth: int = 3, device: int = 0) -> dict:
+    """Per-frame velocity fields of the sequence in ``input_dir``
+    (cli._cmd_flow, cli.py:312-357): ``velocity.f32`` + ``velocity.json``
+    (fmt "f32") or ``velocity.csv`` rows "frame,y,x,vx,vy" over the anchor
+    region (fmt "csv"); frames are numbered by input index."""
+    if fmt not in ("f32", "csv"):
+        raise ValueError(f"unknown flow format {fmt!r}")
+    params = default_params() if params is None else params
+    out_dir = Path(out_dir)
+    with SequenceReader(input_dir) as reader:
+        h, w = reader.shape
+        hdr = reader.header
+        out_dir.mkdir(parents=True, exist_ok=True)
+        fh = open(out_dir / ("velocity.f32" if fmt == "f32" else "velocity.csv"), "w" + ("b" if fmt == "f32" else ""),
+                  **({} if fmt == "f32" else {"encoding": "utf-8"}))
+        if fmt == "csv":
+            fh.write("frame,y,x,vx,vy\n")
+        first, count = [None], [0]
+        ys, xs = np.mgrid[params.my - 1:h, params.mx - 1:w]
+        with Pipeline(params, w, h, device=device) as pipe:
+            lut_v = pipe._lut_v.astype("<f4")
+
+            def consume(_fidx, t_in, _res, _pred, vidx, _stats):
+                vel = np.take(lut_v, vidx.view(np.uint16).reshape(h, w), axis=0)
+                if first[0] is None:
+                    first[0] = t_in
+                count[0] += 1
+                if fmt == "f32":
+                    fh.write(vel.data)
+                else:
+                    va = vel[params.my - 1:, params.mx - 1:]
+                    fh.write("".join(f"{t_in},{y},{x},{vx:.6g},{vy:.6g}\n" for y, x, vx, vy in
+                                     zip(ys.ravel().tolist(), xs.ravel().tolist(),
+                                         va[..., 0].ravel().tolist(), va[..., 1].ravel().tolist())))
+
+            try:
+                _stream(reader, pipe, consume, want_pred=False, want_stats=False, depth=depth)
+            finally:
+                fh.close()
+    if count[0] == 0:
+        raise SequenceError("sequence shorter than the temporal window")
+    if fmt == "f32":
+        _velocity_sidecar(out_dir, count[0], w, h, first[0])
+    return _run_meta(out_dir, {
+        "command": "flow", "params": params_as_dict(params), "strategy": "serial", "input": str(input_dir),
+        "input_seed": hdr.meta.get("seed"), "frames_in": len(reader), "fields_out": count[0], "device": "cuda",
+    })
+
+
+def _velocity_sidecar(out_dir: Path, count: int, width: int, height: int, first_index) -> None:
+    """velocity.json next to velocity.f32 (cli.py:211-227)."""
+    with open(out_dir / "velocity.json", "w", encoding="utf-8") as fh:
+        json.dump({"width": width, "height": height, "frame_count": count, "channels": 2,
+                   "components": ["vx", "vy"], "dtype": "f32le", "first_frame_index": first_index}, fh, indent=2)
         fh.write("\n")
-    return meta
+
+
+def _run_meta(out_dir: Path, payload: dict) -> dict:
+    """run_meta.json (cli.py:59-64)."""
+    payload = dict(payload, version=__version__)
+    with open(out_dir / RUN_META_NAME, "w", encoding="utf-8") as fh:
+        json.dump(payload, fh, indent=2, default=float)
+        fh.write("\n")
+    return payload

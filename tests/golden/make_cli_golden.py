@@ -1,4 +1,4 @@
-"""Golden run of the reference's ``clutterwhiten simulate`` + ``filter``.
+"""Golden run of the reference's ``clutterwhiten simulate`` + ``filter`` + ``flow``.
 
 Run in the build container (the reference is importable only there):
 
@@ -7,8 +7,8 @@ Run in the build container (the reference is importable only there):
 
 Runs the reference CLI (cli.main) exactly as its own test_cli.py does
 (32x32, 12 frames, seed 7; filter with --metrics --emit-prediction
---emit-velocity) and stores the input sequence, ground truth and every
-output file's content in ``cli_filter.npz``.  tests/test_sequence_gpu.py
+--emit-velocity; flow in f32 and csv formats) and stores the input
+sequence, ground truth and every output file's content in ``cli_filter.npz``.  tests/test_sequence_gpu.py
 replays the input through ``filter_sequence`` and compares file by file.
 """
 
@@ -33,6 +33,11 @@ def main_():
                      "--height", "32"]) == 0
         assert main(["filter", "--in", sim, "--out", out, "--metrics", met, "--emit-prediction",
                      "--emit-velocity"]) == 0
+        flow_f32, flow_csv = os.path.join(tmp, "flow"), os.path.join(tmp, "flowcsv")
+        assert main(["flow", "--in", sim, "--out", flow_f32]) == 0
+        assert main(["flow", "--in", sim, "--out", flow_csv, "--format", "csv"]) == 0
+        flow_meta = json.load(open(os.path.join(flow_f32, "run_meta.json")))
+        flow_meta.pop("version", None)
         frames, hin = read_sequence(sim)
         res, hres = read_sequence(out)
         pred, hpred = read_sequence(os.path.join(out, "prediction"))
@@ -51,7 +56,11 @@ def main_():
             residual=res, residual_header=np.frombuffer(json.dumps(hres.to_json_dict()).encode(), np.uint8),
             prediction=pred, prediction_header=np.frombuffer(json.dumps(hpred.to_json_dict()).encode(), np.uint8),
             velocity=vel, velocity_json=text(os.path.join(out, "velocity.json")),
-            metrics=text(met), run_meta=np.frombuffer(json.dumps(run_meta).encode(), np.uint8))
+            metrics=text(met), run_meta=np.frombuffer(json.dumps(run_meta).encode(), np.uint8),
+            flow_velocity=np.fromfile(os.path.join(flow_f32, "velocity.f32"), dtype="<f4"),
+            flow_json=text(os.path.join(flow_f32, "velocity.json")),
+            flow_csv=text(os.path.join(flow_csv, "velocity.csv")),
+            flow_meta=np.frombuffer(json.dumps(flow_meta).encode(), np.uint8))
     print("wrote cli_filter.npz")
 
 

@@ -262,3 +262,36 @@ def test_filter_sequence_vs_reference_cli(params, tmp_path):
         assert fa[0] == fb[0] and fa[3:8] == fb[3:8]  # frame, peak x/y, target x/y, hit
         for i in (1, 2, 8, 9):  # rms, peak value, velocity-error stats (tolerance in the last digit)
             assert abs(float(fa[i]) - float(fb[i])) <= 1e-4 * max(1.0, abs(float(fb[i]))), (i, a, b)
+
+
+@pytest.mark.parametrize("fmt", ["f32", "csv"])
+def test_flow_sequence_vs_reference_cli(params, tmp_path, fmt):
+    """`clutterwhiten flow` (cli.py:312-357) replayed through flow_sequence."""
+    from parity import VEL_FRAC
+
+    from paper_1408_3526_b200.seqio import write_sequence
+    from paper_1408_3526_b200.sequence import flow_sequence
+
+    g = golden("cli_filter.npz")
+    txt = lambda k: g[k].tobytes().decode()
+    write_sequence(g["frames"], tmp_path / "seq", meta=json.loads(txt("input_header"))["meta"])
+    meta = flow_sequence(tmp_path / "seq", tmp_path / "flow", params, fmt=fmt)
+    ref_meta = json.loads(txt("flow_meta"))
+    for k in ("command", "params", "strategy", "input_seed", "frames_in", "fields_out"):
+        assert meta[k] == ref_meta[k], k
+    t = ref_meta["fields_out"]
+    ref = g["flow_velocity"].reshape(t, 32, 32, 2)
+    if fmt == "f32":
+        got = np.fromfile(tmp_path / "flow" / "velocity.f32", dtype="<f4").reshape(t, 32, 32, 2)
+        assert json.loads((tmp_path / "flow" / "velocity.json").read_text()) == json.loads(txt("flow_json"))
+        for k in range(t):
+            a = got[k, params.my - 1:, params.mx - 1:]
+            b = ref[k, params.my - 1:, params.mx - 1:]
+            assert np.all(a == b, axis=-1).mean() >= VEL_FRAC
+    else:
+        lines = (tmp_path / "flow" / "velocity.csv").read_text().split("\n")
+        ref_lines = txt("flow_csv").split("\n")
+        assert lines[0] == ref_lines[0] == "frame,y,x,vx,vy" and len(lines) == len(ref_lines)
+        same = sum(a == b for a, b in zip(lines, ref_lines))
+        assert same >= VEL_FRAC * len(lines)
+        assert [l.split(",")[:3] for l in lines] == [l.split(",")[:3] for l in ref_lines]
