@@ -175,15 +175,54 @@ struct cf {
 __device__ __forceinline__ cf cmk(float r, float i) { return cf{r, i}; }
 __device__ __forceinline__ cf c2(float2 v) { return cf{v.x, v.y}; }
 __device__ __forceinline__ float2 f2(cf v) { return make_float2(v.r, v.i); }
-__device__ __forceinline__ cf cadd(cf a, cf b) { return cf{a.r + b.r, a.i + b.i}; }
-__device__ __forceinline__ cf csub(cf a, cf b) { return cf{a.r - b.r, a.i - b.i}; }
-__device__ __forceinline__ cf cmul(cf a, cf b) { return cf{a.r * b.r - a.i * b.i, a.r * b.i + a.i * b.r}; }
+// Complex arithmetic on packed f32x2 (sm_100 FADD2 / FMUL2 / FFMA2: one
+// instruction for the re and im lanes; scalar operands broadcast for free).
+__device__ __forceinline__ unsigned long long pk(cf a)
+{
+    unsigned long long v;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(v) : "f"(a.r), "f"(a.i));
+    return v;
+}
+__device__ __forceinline__ cf upk(unsigned long long v)
+{
+    cf a;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a.r), "=f"(a.i) : "l"(v));
+    return a;
+}
+__device__ __forceinline__ cf cadd(cf a, cf b)
+{
+    unsigned long long r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk(a)), "l"(pk(b)));
+    return upk(r);
+}
+__device__ __forceinline__ cf csub(cf a, cf b)
+{
+    unsigned long long r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk(a)), "l"(pk(b)));
+    return upk(r);
+}
+// lane-wise a * b + c
+__device__ __forceinline__ cf cfma2(cf a, cf b, cf c)
+{
+    unsigned long long r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk(a)), "l"(pk(b)), "l"(pk(c)));
+    return upk(r);
+}
+__device__ __forceinline__ cf cmul(cf a, cf b)
+{
+    // (a.r b.r - a.i b.i, a.r b.i + a.i b.r) = a.r (b.r, b.i) + a.i (-b.i, b.r)
+    unsigned long long t;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(pk(cf{a.r, a.r})), "l"(pk(b)));
+    return cfma2(cf{a.i, a.i}, cf{-b.i, b.r}, upk(t));
+}
 __device__ __forceinline__ cf cconj(cf a) { return cf{a.r, -a.i}; }
-// 2c - (a + b) = 4 x one tap of the circular (-1/4, 1/2, -1/4) Hann
-// (_kernels.py:177-217); the 4^3 is folded into the kz-collapse table.
+// (a + b) - 2c = -4 x one tap of the circular (-1/4, 1/2, -1/4) Hann
+// (_kernels.py:177-217), exactly the negation of 2c - (a + b): the three
+// passes give -H C, whose power is bit-identical; the 4^3 is folded into
+// the kz-collapse table.  Two packed instructions per complex bin.
 __device__ __forceinline__ cf hann4(cf a, cf c, cf b)
 {
-    return cf{fmaf(2.f, c.r, -(a.r + b.r)), fmaf(2.f, c.i, -(a.i + b.i))};
+    return cfma2(cf{-2.f, -2.f}, c, cadd(a, b));
 }
 
 // Total order of the reference pick (_kernels.py:286-298): larger score,

@@ -22,6 +22,14 @@ struct NaiveArgs {
     int y_begin, y_off;
 };
 
+// scalar complex multiply-accumulate acc + a * b (this kernel is a
+// reference-style direct evaluation; the packed helpers of the frame kernel
+// only raise its register pressure)
+__device__ __forceinline__ cf cmac_s(cf acc, cf a, cf b)
+{
+    return cf{acc.r + (a.r * b.r - a.i * b.i), acc.i + (a.r * b.i + a.i * b.r)};
+}
+
 template <class G>
 __global__ void __launch_bounds__(G::NTHREADS, 1)
 cw_naive_kernel(const NaiveArgs a, const Tables t)
@@ -92,14 +100,14 @@ cw_naive_kernel(const NaiveArgs a, const Tables t)
                 cf acc = cmk(0.f, 0.f);
 #pragma unroll
                 for (int my = 0; my < MY; my++)
-                    acc = cadd(acc, cmul(cmk(t.eyc[r][my], t.eys[r][my]), xfv(mz, my, kx)));
+                    acc = cmac_s(acc, cmk(t.eyc[r][my], t.eys[r][my]), xfv(mz, my, kx));
                 yv[mz] = acc;
             }
 #pragma unroll
             for (int kzi = 0; kzi < MZ; kzi++) {
                 cf acc = cmk(0.f, 0.f);
 #pragma unroll
-                for (int mz = 0; mz < MZ; mz++) acc = cadd(acc, cmul(tphase(kzi - KZ, mz), yv[mz]));
+                for (int mz = 0; mz < MZ; mz++) acc = cmac_s(acc, tphase(kzi - KZ, mz), yv[mz]);
                 out[kzi] = anchor ? acc : cmk(0.f, 0.f);
             }
         };
