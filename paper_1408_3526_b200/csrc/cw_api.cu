@@ -210,6 +210,7 @@ static void build_tables(cw_handle *h)
         for (int m = 0; m < Mx; m++) {
             t.exc[k][m] = (float)std::cos(2 * PI * k * m / Mx);
             t.exs[k][m] = (float)std::sin(2 * PI * k * m / Mx);
+            t.ex2[k][m] = make_float2(t.exc[k][m], t.exs[k][m]);
         }
     for (int k = 0; k <= h->ky; k++) {
         for (int m = 0; m < My; m++) {
@@ -218,6 +219,8 @@ static void build_tables(cw_handle *h)
         }
         t.twc[k] = (float)std::cos(2 * PI * k / My);
         t.tws[k] = (float)std::sin(2 * PI * k / My);
+        t.tw2[k] = make_float2(t.twc[k], t.tws[k]);
+        t.twn2[k] = make_float2(-t.tws[k], t.twc[k]);
     }
     // S = norm * z+; the three unscaled Hann passes each scale by 4, so
     // P = |C|^2 = norm^2 / 4^6 |C_unscaled|^2: fold into the kz collapse.
@@ -229,6 +232,9 @@ static void build_tables(cw_handle *h)
         t.ws[i] = (float)std::sin(2 * PI * kz / Mz);
         t.azc[i] = (float)(pscale * std::cos(2 * PI * kz / Mz));
         t.azs[i] = (float)(-pscale * std::sin(2 * PI * kz / Mz));
+        t.w2[i] = make_float2(t.wc[i], t.ws[i]);
+        t.wn2[i] = make_float2(-t.ws[i], t.wc[i]);
+        t.az2[i] = make_float2(t.azc[i], t.azs[i]);
     }
     std::vector<double> gx(h->nlx), gy(h->nly);
     for (int i = 0; i < h->nlx; i++)

@@ -55,6 +55,12 @@ struct Tables {
     // kz collapse a_z(kz) = exp(-j 2 pi kz / Mz), index kz + KZ, times
     // norm^2 / 4096 (the three unscaled Hann passes each carry a factor 4)
     float azc[MAXM], azs[MAXM];
+    // the same constants as (re, im) pairs for the packed f32x2 paths:
+    // ex2 = (exc, exs); w2 = (wc, ws), wn2 = (-ws, wc); az2 = (azc, azs);
+    // tw2 / twn2 likewise for the y resonators
+    float2 ex2[MAXK + 1][MAXM];
+    float2 w2[MAXM], wn2[MAXM], az2[MAXM];
+    float2 tw2[MAXK + 1], twn2[MAXK + 1];
     // lag-contraction coefficients, one 16-byte aligned record per lag:
     // [0] = gain, [1..MAXK] = cos terms, [MAXK+1..2 MAXK] = sin terms.
     // stage 1 (gx folded): B(ky,lx) = g*T(0) + sum_kx c*A - j s*D
@@ -215,6 +221,21 @@ __device__ __forceinline__ cf cmul(cf a, cf b)
     asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(pk(cf{a.r, a.r})), "l"(pk(b)));
     return cfma2(cf{a.i, a.i}, cf{-b.i, b.r}, upk(t));
 }
+// z * w for a constant w supplied as the pairs w = (wr, wi), wn = (-wi, wr):
+// z.r (wr, wi) + z.i (-wi, wr), two packed instructions
+__device__ __forceinline__ cf cmulw(cf z, float2 w, float2 wn)
+{
+    unsigned long long t;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(pk(cf{z.r, z.r})), "l"(pk(cf{w.x, w.y})));
+    return cfma2(cf{z.i, z.i}, cf{wn.x, wn.y}, upk(t));
+}
+// lane-wise a * b
+__device__ __forceinline__ cf cmul2(cf a, cf b)
+{
+    unsigned long long t;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(pk(a)), "l"(pk(b)));
+    return upk(t);
+}
 __device__ __forceinline__ cf cconj(cf a) { return cf{a.r, -a.i}; }
 // (a + b) - 2c = -4 x one tap of the circular (-1/4, 1/2, -1/4) Hann
 // (_kernels.py:177-217), exactly the negation of 2c - (a + b): the three
@@ -328,7 +349,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
         srxy[2 * i] = t.rix[i];
         srxy[2 * i + 1] = t.riy[i];
     }
-    const cf tw_r = cmk(t.twc[threadIdx.x >> 5], t.tws[threadIdx.x >> 5]);  // this warp's y resonator
+    const float2 tw_r = t.tw2[threadIdx.x >> 5], twn_r = t.twn2[threadIdx.x >> 5];  // this warp's y resonator
     uint64_t *bar_t = bar + 1;  // bar: observer-state packet, bar_t: T^ packet
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
@@ -365,48 +386,40 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
 
 #define XFR(slot, f) xfr[((slot) * G::XF + (f)) * 32 + lane]
 
-    // x stage for local row yy at column x: Mx-tap window sums (the row
-    // sweep, _kernels.py:31-45), zero outside the frame; kx = 0 real.
-    auto xstage = [&](int yy, int x, int slot) {
-        float acc[G::XF];
+    // x stage: Mx-tap window sums of a frame row at this lane's column (the
+    // row sweep, _kernels.py:31-45), zero outside the frame; kx = 0 real,
+    // kx >= 1 accumulated as packed (cos, sin) pairs
+    auto xsum_store = [&](int slot, auto &&sample) {
+        float dc = 0.f;
+        cf acc[KX + 1];
 #pragma unroll
-        for (int f = 0; f < G::XF; f++) acc[f] = 0.f;
-        if (yy >= 0 && yy < H) {
-            const float *row = a.frame + (size_t)yy * W;
-#pragma unroll
-            for (int m = 0; m < MX; m++) {
-                const int xx = x - m;
-                const float v = (xx >= 0 && xx < W) ? __ldg(row + xx) : 0.f;
-                acc[0] += v;
-#pragma unroll
-                for (int k = 1; k <= KX; k++) {
-                    acc[2 * k - 1] = fmaf(t.exc[k][m], v, acc[2 * k - 1]);
-                    acc[2 * k] = fmaf(t.exs[k][m], v, acc[2 * k]);
-                }
-            }
-        }
-#pragma unroll
-        for (int f = 0; f < G::XF; f++) XFR(slot, f) = acc[f];
-    };
-    // same sums from the row segment prefetched into rowbuf (cp.async):
-    // rowbuf[i] = frame[row][x0 - (MX-1) + i], zero outside the frame
-    auto xstage_s = [&](int slot) {
-        float acc[G::XF];
-#pragma unroll
-        for (int f = 0; f < G::XF; f++) acc[f] = 0.f;
+        for (int k = 1; k <= KX; k++) acc[k] = cmk(0.f, 0.f);
 #pragma unroll
         for (int m = 0; m < MX; m++) {
-            const float v = rowbuf[lane + MX - 1 - m];
-            acc[0] += v;
+            const float v = sample(m);
+            dc += v;
 #pragma unroll
-            for (int k = 1; k <= KX; k++) {
-                acc[2 * k - 1] = fmaf(t.exc[k][m], v, acc[2 * k - 1]);
-                acc[2 * k] = fmaf(t.exs[k][m], v, acc[2 * k]);
-            }
+            for (int k = 1; k <= KX; k++) acc[k] = cfma2(c2(t.ex2[k][m]), cf{v, v}, acc[k]);
         }
+        XFR(slot, 0) = dc;
 #pragma unroll
-        for (int f = 0; f < G::XF; f++) XFR(slot, f) = acc[f];
+        for (int k = 1; k <= KX; k++) {
+            XFR(slot, 2 * k - 1) = acc[k].r;
+            XFR(slot, 2 * k) = acc[k].i;
+        }
     };
+    // for local row yy from global memory (prologue / warm-up frames)
+    auto xstage = [&](int yy, int x, int slot) {
+        const bool rv = yy >= 0 && yy < H;
+        const float *row = a.frame + (size_t)(rv ? yy : 0) * W;
+        xsum_store(slot, [&](int m) {
+            const int xx = x - m;
+            return (rv && xx >= 0 && xx < W) ? __ldg(row + xx) : 0.f;
+        });
+    };
+    // from the row segment prefetched into rowbuf (cp.async):
+    // rowbuf[i] = frame[row][x0 - (MX-1) + i], zero outside the frame
+    auto xstage_s = [&](int slot) { xsum_store(slot, [&](int m) { return rowbuf[lane + MX - 1 - m]; }); };
     auto prefetch_row = [&](int yy, int x0) {  // async: the next row's 32 + MX - 1 samples
         const bool rv = yy >= 0 && yy < H;
         const float *row = a.frame + (size_t)(rv ? yy : 0) * W;
@@ -476,7 +489,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                 // comb + resonator (_kernels.py:62-68)
                 const int s1 = ring_slot(yy), s0 = ring_slot(yy - MY);
 #pragma unroll
-                for (int i = 0; i < MX; i++) sp[i] = cadd(cmul(tw_r, sp[i]), csub(xfv(s1, i - KX), xfv(s0, i - KX)));
+                for (int i = 0; i < MX; i++) sp[i] = cadd(cmulw(sp[i], tw_r, twn_r), csub(xfv(s1, i - KX), xfv(s0, i - KX)));
             }
             const bool anchor = colv && x >= MX - 1 && (yy + a.y_off) >= MY - 1;
             const size_t pix = (size_t)yy * NXB + xb;
@@ -508,7 +521,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
 #pragma unroll
                     for (int kz = 1; kz <= KZ; kz++) {
                         const cf zp = cmk(zd[kz].r + e, zd[kz].i);
-                        stg[kz * 32] = f2(cmul(cmk(t.wc[kz + KZ], t.ws[kz + KZ]), zp));
+                        stg[kz * 32] = f2(cmulw(zp, t.w2[kz + KZ], t.wn2[kz + KZ]));
                         sret[kz * 32 + lane] = f2(zp);
                     }
                 }
@@ -526,12 +539,12 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                         z[kzi] = c2(sst[(base + kzi) * 32]);
                         sum = cadd(sum, z[kzi]);
                     }
-                    const cf e = cmk(fmaf(-t.inv_mz, sum.r, uv.r), fmaf(-t.inv_mz, sum.i, uv.i));
+                    const cf e = cfma2(cf{-t.inv_mz, -t.inv_mz}, sum, uv);
                     cf zp[MZ];
 #pragma unroll
                     for (int kzi = 0; kzi < MZ; kzi++) {
                         zp[kzi] = cadd(z[kzi], e);
-                        const cf zn = (kzi == KZ) ? zp[kzi] : cmul(cmk(t.wc[kzi], t.ws[kzi]), zp[kzi]);
+                        const cf zn = (kzi == KZ) ? zp[kzi] : cmulw(zp[kzi], t.w2[kzi], t.wn2[kzi]);
                         stg[(base + kzi) * 32] = f2(zn);
                         if (kx <= BX) sret[(base + kzi) * 32 + lane] = f2(zp[kzi]);
                     }
@@ -572,13 +585,13 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                         z[kzi] = c2(sst[(kxi * MZ + kzi) * 32]);
                         sum = cadd(sum, z[kzi]);
                     }
-                    const cf e = cmk(fmaf(-t.inv_mz, sum.r, uv.r), fmaf(-t.inv_mz, sum.i, uv.i));
+                    const cf e = cfma2(cf{-t.inv_mz, -t.inv_mz}, sum, uv);
                     cf zp[MZ];
                     const int kxb = kxi - KX + BX;  // retained-band column
 #pragma unroll
                     for (int kzi = 0; kzi < MZ; kzi++) {
                         zp[kzi] = cadd(z[kzi], e);
-                        const cf zn = (kzi == KZ) ? zp[kzi] : cmul(cmk(t.wc[kzi], t.ws[kzi]), zp[kzi]);
+                        const cf zn = (kzi == KZ) ? zp[kzi] : cmulw(zp[kzi], t.w2[kzi], t.wn2[kzi]);
                         stg[(kxi * MZ + kzi) * 32] = f2(zn);
                         if (r <= BY && kxb >= 0 && kxb < G::WX) rr[(kxb * MZ + kzi) * 32] = f2(zp[kzi]);
                     }
@@ -629,8 +642,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                             const cf up = cconj(cx_at(1, -kz, -kx));
                             const cf c = hann4(up, cx_at(0, kz, kx), cx_at(1, kz, kx));
                             const float p = fmaf(c.r, c.r, c.i * c.i);
-                            acc.r = fmaf(t.azc[kz + KZ], p, acc.r);
-                            acc.i = fmaf(t.azs[kz + KZ], p, acc.i);
+                            acc = cfma2(c2(t.az2[kz + KZ]), cf{p, p}, acc);
                         }
                         T[KX + kx] = acc;
                     }
@@ -646,8 +658,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                             const cf dn = (r < KY) ? cx_at(r + 1, kz, kx) : cconj(cx_at(KY, -kz, -kx));
                             const cf c = hann4(up, cx_at(r, kz, kx), dn);
                             const float p = fmaf(c.r, c.r, c.i * c.i);
-                            acc.r = fmaf(t.azc[kzi], p, acc.r);
-                            acc.i = fmaf(t.azs[kzi], p, acc.i);
+                            acc = cfma2(c2(t.az2[kzi]), cf{p, p}, acc);
                         }
                         T[kxi] = acc;
                     }
@@ -666,7 +677,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                     if (r == 0 && kxi == KX) v2.i = 0.f;  // T(0,0) is real
                     if (!a.first) {
                         const float2 o = tho[j * 32];
-                        v2 = cmk(fmaf(t.beta, v2.r, t.alpha * o.x), fmaf(t.beta, v2.i, t.alpha * o.y));
+                        v2 = cfma2(cf{t.beta, t.beta}, v2, cmul2(cf{t.alpha, t.alpha}, c2(o)));
                     }
                     thg[j * 32] = f2(v2);
                     tho[j * 32] = f2(v2);
@@ -856,21 +867,22 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                 // stored half space: pred = sum_j coef[v][j] . z+[j]
                 const float2 *cp = a.coefP + (size_t)(viy * nlx + vix) * G::RETP + G::ppair(r);
                 const float2 *sr = sret + G::ppair(r) * 32 + lane;
-                float acc[4] = {0.f, 0.f, 0.f, 0.f};
+                cf acc[2] = {cmk(0.f, 0.f), cmk(0.f, 0.f)};  // packed (c.x z.x, c.y z.y) partial sums
                 if (r == 0) {
 #pragma unroll
                     for (int j = 0; j < G::PROW0P; j++) {
                         const float2 c = __ldg(cp + j), z = sr[j * 32];
-                        acc[j & 3] = fmaf(c.x, z.x, fmaf(c.y, z.y, acc[j & 3]));
+                        acc[j & 1] = cfma2(c2(c), c2(z), acc[j & 1]);
                     }
                 } else {
 #pragma unroll
                     for (int j = 0; j < G::PROWNP; j++) {
                         const float2 c = __ldg(cp + j), z = sr[j * 32];
-                        acc[j & 3] = fmaf(c.x, z.x, fmaf(c.y, z.y, acc[j & 3]));
+                        acc[j & 1] = cfma2(c2(c), c2(z), acc[j & 1]);
                     }
                 }
-                ppef[r * 32 + lane] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+                const cf sum = cadd(acc[0], acc[1]);
+                ppef[r * 32 + lane] = sum.r + sum.i;
             }
             if (r == 0 && colv) {
                 uint8_t *vp = a.vidx + ((size_t)yy * W + x) * 2;
