@@ -243,20 +243,20 @@ static void build_tables(cw_handle *h)
         gy[i] = 0.375 / (0.25 + 0.125 * std::cos(2 * PI * h->lag_y[i] / My));
     // stage 1: e^{-j 2 pi kx lx / Mx} = cos - j sin, gx folded
     for (int l = 0; l < h->nlx; l++) {
-        t.s1v[l][0] = (float)gx[l];
+        t.s1v[l].gain = (float)gx[l];
         for (int k = 1; k <= h->kx; k++) {
             const double th = 2 * PI * k * h->lag_x[l] / Mx;
-            t.s1v[l][k] = (float)(gx[l] * std::cos(th));
-            t.s1v[l][MAXK + k] = (float)(gx[l] * std::sin(th));
+            t.s1v[l].cs[k - 1].x = (float)(gx[l] * std::cos(th));
+            t.s1v[l].cs[k - 1].y = (float)(gx[l] * std::sin(th));
         }
     }
     // stage 2: R = B0 + 2 sum_ky (cos phi Re B + sin phi Im B), gy folded
     for (int l = 0; l < h->nly; l++) {
-        t.s2v[l][0] = (float)gy[l];
+        t.s2v[l].gain = (float)gy[l];
         for (int k = 1; k <= h->ky; k++) {
             const double ph = 2 * PI * k * h->lag_y[l] / My;
-            t.s2v[l][k] = (float)(2.0 * gy[l] * std::cos(ph));
-            t.s2v[l][MAXK + k] = (float)(2.0 * gy[l] * std::sin(ph));
+            t.s2v[l].cs[k - 1].x = (float)(2.0 * gy[l] * std::cos(ph));
+            t.s2v[l].cs[k - 1].y = (float)(2.0 * gy[l] * std::sin(ph));
         }
     }
     // rank: sort by (lag_x^2 + lag_y^2, ix, iy) -- the reference tie order

@@ -43,6 +43,12 @@ constexpr int RESTART = 32;  // rows between direct y-SDFT restarts (bounds f32 
 #define CW_FENCE_ALL 1  // every thread orders its generic stage reads before the next TMA write
 #endif
 
+struct alignas(16) LagRec {
+    float gain, pad;
+    float2 cs[MAXK];  // cs[k - 1] = (cos, sin) coefficient of frequency k
+};
+static_assert(sizeof(LagRec) == 4 * LREC, "lag record layout");
+
 struct Tables {
     // x stage: cos/sin(2 pi kx m / Mx), kx = 0..KX, m = 0..Mx-1
     float exc[MAXK + 1][MAXM], exs[MAXK + 1][MAXM];
@@ -61,12 +67,12 @@ struct Tables {
     float2 ex2[MAXK + 1][MAXM];
     float2 w2[MAXM], wn2[MAXM], az2[MAXM];
     float2 tw2[MAXK + 1], twn2[MAXK + 1];
-    // lag-contraction coefficients, one 16-byte aligned record per lag:
-    // [0] = gain, [1..MAXK] = cos terms, [MAXK+1..2 MAXK] = sin terms.
+    // lag-contraction coefficients, one 16-byte aligned record per lag
+    // (LagRec: gain, then the (cos, sin) pair of each frequency k = 1..MAXK).
     // stage 1 (gx folded): B(ky,lx) = g*T(0) + sum_kx c*A - j s*D
     // stage 2 (gy and the factor 2 folded): R = g B0 + sum_ky c Re B + s Im B
-    alignas(16) float s1v[MAXL][LREC];
-    alignas(16) float s2v[MAXL][LREC];
+    LagRec s1v[MAXL];
+    LagRec s2v[MAXL];
     // argmax total order: rank[ly * nlx + lx]; rank -> (ix, iy)
     uint16_t rank[MAXL * MAXL];
     uint8_t rix[MAXL * MAXL], riy[MAXL * MAXL];
@@ -703,27 +709,27 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                     }
                     return c2(tstage[(G::tpair(ky) + kx + KX) * 32 + lane]);
                 };
-                // stage 2 + in-column argmax for one column whose B values are given
-                auto column = [&](int lx, float b0, const float *br, const float *bi) {
+                // stage 2 + in-column argmax for one column whose B values
+                // are given: b0 = B(0, lx) (real), bq[ky] = B(ky, lx), ky >= 1
+                auto column = [&](int lx, float b0, const cf *bq) {
                     if (NL && t.sym_y) {
                         // visit ly = 0, -1, +1, -2, +2, ...: ascending rank order within
                         // a column (|v|^2 grows with |ly|, then iy ascending); two
                         // interleaved chains (q odd / even) for ILP, each strict '>',
                         // merged by visit index -> the reference's tie winner
                         constexpr int C0 = NL / 2;
-                        float ca = -INFINITY, cb = t.s2v[C0][0] * b0;
+                        float ca = -INFINITY, cb = t.s2v[C0].gain * b0;
 #pragma unroll
-                        for (int k = 1; k <= KY; k++) cb = fmaf(t.s2v[C0][k], br[k], cb);
+                        for (int k = 1; k <= KY; k++) cb = fmaf(t.s2v[C0].cs[k - 1].x, bq[k].r, cb);
                         int ia = 0x7fff, ib = 0;
 #pragma unroll
                         for (int q = 1; q <= C0; q++) {
-                            float e = t.s2v[C0 + q][0] * b0, o = 0.f;
+                            // (e, o) = (g b0 + sum c Re B, sum s Im B); (vm, vp) = e -+ o
+                            cf eo = cmk(t.s2v[C0 + q].gain * b0, 0.f);
 #pragma unroll
-                            for (int k = 1; k <= KY; k++) {
-                                e = fmaf(t.s2v[C0 + q][k], br[k], e);
-                                o = fmaf(t.s2v[C0 + q][MAXK + k], bi[k], o);
-                            }
-                            const float vm = e - o, vp = e + o;
+                            for (int k = 1; k <= KY; k++) eo = cfma2(c2(t.s2v[C0 + q].cs[k - 1]), bq[k], eo);
+                            const cf v = cfma2(cf{eo.i, eo.i}, cf{-1.f, 1.f}, cf{eo.r, eo.r});
+                            const float vm = v.r, vp = v.i;
                             if (q & 1) {
                                 if (vm > ca) { ca = vm; ia = 2 * q - 1; }
                                 if (vp > ca) { ca = vp; ia = 2 * q; }
@@ -738,12 +744,10 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                         if (better(cb, rk, best, brk)) { best = cb; brk = rk; }
                     } else {
                         for (int ly = 0; ly < nly; ly++) {
-                            float v = t.s2v[ly][0] * b0;
+                            cf acc = cmk(t.s2v[ly].gain * b0, 0.f);
 #pragma unroll
-                            for (int k = 1; k <= KY; k++) {
-                                v = fmaf(t.s2v[ly][k], br[k], v);
-                                v = fmaf(t.s2v[ly][MAXK + k], bi[k], v);
-                            }
+                            for (int k = 1; k <= KY; k++) acc = cfma2(c2(t.s2v[ly].cs[k - 1]), bq[k], acc);
+                            const float v = acc.r + acc.i;
                             const int rk = srank[ly * nlx + lx];
                             if (better(v, rk, best, brk)) { best = v; brk = rk; }
                         }
@@ -753,58 +757,50 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                     // +-lx pairing: this warp owns |lx| = C0 + q for q = r, r + NR, ...
                     constexpr int C0 = NL / 2;
                     for (int q = r; q <= C0; q += NR) {
-                        const int lp = C0 + q;
-                        const float g = t.s1v[lp][0];
-                        float c1[KX + 1], s1[KX + 1];
+                        const LagRec &L = t.s1v[C0 + q];
+                        const float g = L.gain;
+                        float bp0, bm0;
+                        cf bqp[KY + 1], bqm[KY + 1];  // B(ky, +-lx)
+                        {   // row 0: T(0,-kx) = conj T(0,kx):
+                            // B(0, +-lx) = g T00 + 2 sum c Re T -+ 2 sum s Im T
+                            cf acc = cmk(0.f, 0.f);
 #pragma unroll
-                        for (int kx = 1; kx <= KX; kx++) {
-                            c1[kx] = t.s1v[lp][kx];
-                            s1[kx] = t.s1v[lp][MAXK + kx];
-                        }
-                        float bp0, bm0, brp[KY + 1], bip[KY + 1], brm[KY + 1], bim[KY + 1];
-                        {   // row 0: T(0,-kx) = conj T(0,kx)
-                            float cp = g * tv(0, 0).r, sp2 = 0.f;
-#pragma unroll
-                            for (int kx = 1; kx <= KX; kx++) {
-                                const cf v = tv(0, kx);
-                                cp = fmaf(2.f * c1[kx], v.r, cp);
-                                sp2 = fmaf(2.f * s1[kx], v.i, sp2);
-                            }
-                            bp0 = cp + sp2;
-                            bm0 = cp - sp2;
+                            for (int kx = 1; kx <= KX; kx++) acc = cfma2(c2(L.cs[kx - 1]), tv(0, kx), acc);
+                            const float cp = fmaf(2.f, acc.r, g * tv(0, 0).r);
+                            bp0 = fmaf(2.f, acc.i, cp);
+                            bm0 = fmaf(-2.f, acc.i, cp);
                         }
 #pragma unroll
                         for (int ky = 1; ky <= KY; ky++) {
-                            const cf t0 = tv(ky, 0);
-                            float cr = g * t0.r, ci = g * t0.i, sr = 0.f, si = 0.f;
+                            // P = (cr, ci) = g T0 + sum c A; Q = (sr, -si) = sum s (D.i, D.r)
+                            cf P = cmul2(cf{g, g}, tv(ky, 0)), Q = cmk(0.f, 0.f);
 #pragma unroll
                             for (int kx = 1; kx <= KX; kx++) {
                                 const cf tp = tv(ky, kx), tm = tv(ky, -kx);
                                 const cf A = cadd(tp, tm), D = csub(tp, tm);
-                                cr = fmaf(c1[kx], A.r, cr);
-                                ci = fmaf(c1[kx], A.i, ci);
-                                sr = fmaf(s1[kx], D.i, sr);
-                                si = fmaf(-s1[kx], D.r, si);
+                                const float c = L.cs[kx - 1].x, sn = L.cs[kx - 1].y;
+                                P = cfma2(cf{c, c}, A, P);
+                                Q = cfma2(cf{sn, sn}, cf{D.i, D.r}, Q);
                             }
-                            brp[ky] = cr + sr;
-                            bip[ky] = ci + si;
-                            brm[ky] = cr - sr;
-                            bim[ky] = ci - si;
+                            bqp[ky] = cfma2(Q, cf{1.f, -1.f}, P);   // (cr + sr, ci + si)
+                            bqm[ky] = cfma2(Q, cf{-1.f, 1.f}, P);   // (cr - sr, ci - si)
                         }
-                        column(C0 + q, bp0, brp, bip);
-                        if (q) column(C0 - q, bm0, brm, bim);
+                        column(C0 + q, bp0, bqp);
+                        if (q) column(C0 - q, bm0, bqm);
                     }
                 } else {
                     for (int lx = r; lx < nlx; lx += NR) {
-                        const float g = t.s1v[lx][0];
-                        float b0, br[KY + 1], bi[KY + 1];
+                        const LagRec &L = t.s1v[lx];
+                        const float g = L.gain;
+                        float b0;
+                        cf bq[KY + 1];
                         {
                             float b = g * tv(0, 0).r;
 #pragma unroll
                             for (int kx = 1; kx <= KX; kx++) {
                                 const cf v = tv(0, kx);
-                                b = fmaf(2.f * t.s1v[lx][kx], v.r, b);
-                                b = fmaf(2.f * t.s1v[lx][MAXK + kx], v.i, b);
+                                b = fmaf(2.f * L.cs[kx - 1].x, v.r, b);
+                                b = fmaf(2.f * L.cs[kx - 1].y, v.i, b);
                             }
                             b0 = b;
                         }
@@ -816,14 +812,13 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                             for (int kx = 1; kx <= KX; kx++) {
                                 const cf tp = tv(ky, kx), tm = tv(ky, -kx);
                                 const cf A = cadd(tp, tm), D = csub(tp, tm);
-                                const float c = t.s1v[lx][kx], s = t.s1v[lx][MAXK + kx];
-                                xr = fmaf(c, A.r, fmaf(s, D.i, xr));
-                                xi = fmaf(c, A.i, fmaf(-s, D.r, xi));
+                                const float c = L.cs[kx - 1].x, sn = L.cs[kx - 1].y;
+                                xr = fmaf(c, A.r, fmaf(sn, D.i, xr));
+                                xi = fmaf(c, A.i, fmaf(-sn, D.r, xi));
                             }
-                            br[ky] = xr;
-                            bi[ky] = xi;
+                            bq[ky] = cmk(xr, xi);
                         }
-                        column(lx, b0, br, bi);
+                        column(lx, b0, bq);
                     }
                 }
                 pbest[r * 32 + lane] = make_float2(best, __int_as_float(brk));
