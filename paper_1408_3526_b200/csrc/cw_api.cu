@@ -80,19 +80,27 @@ bool find_inst(int kx, int ky, int kz, int bx, int by, int nl_sym, LaunchFn *out
     if (kx == a && ky == b && kz == c && bx == d && by == e) {                 \
         const int nls[] = {__VA_ARGS__};                                        \
         (void)nls;                                                              \
-        CW_NL(a, b, c, d, e, 9) CW_NL(a, b, c, d, e, 17) CW_NL(a, b, c, d, e, 33) \
+        CW_NLS(a, b, c, d, e)                                                   \
         *out = make_inst<a, b, c, d, e, 0>();                                   \
         return true;                                                            \
     }
+#ifdef CW_DEV_DEFAULT_ONLY
+#define CW_NLS(a, b, c, d, e) CW_NL(a, b, c, d, e, 17)
+#else
+#define CW_NLS(a, b, c, d, e) CW_NL(a, b, c, d, e, 9) CW_NL(a, b, c, d, e, 17) CW_NL(a, b, c, d, e, 33)
+#endif
 #define CW_NL(a, b, c, d, e, n)                                                 \
     if (nl_sym == n) {                                                          \
         *out = make_inst<a, b, c, d, e, n>();                                   \
         return true;                                                            \
     }
     CW_GEO(4, 4, 2, 3, 3, 0)
+#ifndef CW_DEV_DEFAULT_ONLY  // dev builds (tools/dev_build.sh): default geometry, 17 lags only
     CW_GEO(3, 3, 2, 2, 2, 0)
     CW_GEO(5, 5, 2, 4, 4, 0)
     CW_GEO(4, 4, 1, 3, 3, 0)
+#endif
+#undef CW_NLS
 #undef CW_NL
 #undef CW_GEO
     return false;
