@@ -632,61 +632,94 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                 cp_async4(delbuf + lane, anchor ? a.delayed + o : a.frame, anchor);
             }
             // ---------------- phase C1: Hy, power, kz collapse, smoothing ----------------
-            // T^ of this warp's row -> HBM and, in place, to the T^ stage where
-            // every warp reads all rows for the lag contraction
+            // Column ownership (a transpose through shared memory): warp r owns
+            // the spatial-frequency columns kx = +-c, c = r, r + NR, ..., over
+            // all rows ky, so Hy reads every Cx value once (rows were owned in
+            // phase B, where Hx ran in registers).  Its T^ values go to HBM
+            // and, in place, to the T^ stage every warp reads in phase CD.
             {
-                float2 *thg = a.that + (pix * G::NTP + G::tpair(r)) * 32 + lane;
-                float2 *tho = tstage + G::tpair(r) * 32 + lane;
-                cf T[MX];
-                if (r == 0) {
-#pragma unroll
-                    for (int kx = 0; kx <= KX; kx++) {
-                        cf acc = cmk(0.f, 0.f);
-#pragma unroll
-                        for (int kz = -KZ; kz <= KZ; kz++) {
-                            // row -1 = conj-flip of row 1
-                            const cf up = cconj(cx_at(1, -kz, -kx));
-                            const cf c = hann4(up, cx_at(0, kz, kx), cx_at(1, kz, kx));
-                            const float p = fmaf(c.r, c.r, c.i * c.i);
-                            acc = cfma2(c2(t.az2[kz + KZ]), cf{p, p}, acc);
-                        }
-                        T[KX + kx] = acc;
-                    }
-                } else {
-#pragma unroll
-                    for (int kxi = 0; kxi < MX; kxi++) {
-                        cf acc = cmk(0.f, 0.f);
-#pragma unroll
-                        for (int kzi = 0; kzi < MZ; kzi++) {
-                            const int kz = kzi - KZ, kx = kxi - KX;
-                            const cf up = cx_at(r - 1, kz, kx);
-                            // row KY+1 == -KY = conj-flip of row KY
-                            const cf dn = (r < KY) ? cx_at(r + 1, kz, kx) : cconj(cx_at(KY, -kz, -kx));
-                            const cf c = hann4(up, cx_at(r, kz, kx), dn);
-                            const float p = fmaf(c.r, c.r, c.i * c.i);
-                            acc = cfma2(c2(t.az2[kzi]), cf{p, p}, acc);
-                        }
-                        T[kxi] = acc;
-                    }
-                }
-                // smoothing of T^ (_kernels.py:261-271; first ready frame copies)
-                if (use_that) {
+                if (use_that) {  // T^ packet staged (TMA issued after barrier 3 of the last row)
                     mbar_wait(bar_t, phase_t);
                     phase_t ^= 1;
                 }
-                const int k0 = (r == 0) ? KX : 0;
-#pragma unroll
-                for (int kxi = 0; kxi < MX; kxi++) {
-                    if (kxi < k0) continue;
-                    const int j = (r == 0) ? kxi - KX : kxi;  // pair index within the row
-                    cf v2 = T[kxi];
-                    if (r == 0 && kxi == KX) v2.i = 0.f;  // T(0,0) is real
+                float2 *thg = a.that + pix * G::NTP * 32 + lane;
+                // smoothing of T^ (_kernels.py:261-271; first ready frame copies)
+                auto smooth = [&](int j, cf v2) {
                     if (!a.first) {
-                        const float2 o = tho[j * 32];
+                        const float2 o = tstage[j * 32 + lane];
                         v2 = cfma2(cf{t.beta, t.beta}, v2, cmul2(cf{t.alpha, t.alpha}, c2(o)));
                     }
                     thg[j * 32] = f2(v2);
-                    tho[j * 32] = f2(v2);
+                    tstage[j * 32 + lane] = f2(v2);
+                };
+                // 4^3 x the Hann-conditioned power, collapsed over kz with a_z
+                // (up, centre, down rows of one column; kz index kzi)
+                auto tcol = [&](const cf *up, const cf *ce, const cf *dn) -> cf {
+                    cf acc = cmk(0.f, 0.f);
+#pragma unroll
+                    for (int kzi = 0; kzi < MZ; kzi++) {
+                        const cf c = hann4(up[kzi], ce[kzi], dn[kzi]);
+                        const float p = fmaf(c.r, c.r, c.i * c.i);
+                        acc = cfma2(c2(t.az2[kzi]), cf{p, p}, acc);
+                    }
+                    return acc;
+                };
+                auto flip = [&](cf *dst, const cf *src) {  // conj(C(-kz)): the mirrored row/column
+#pragma unroll
+                    for (int kzi = 0; kzi < MZ; kzi++) dst[kzi] = cconj(src[MZ - 1 - kzi]);
+                };
+                for (int c = r; c <= KX; c += NR) {
+                    if (c == 0) {
+                        // column kx = 0: rows 0..KY; C(0, 0, -kz) = conj C(0, 0, kz)
+                        cf v[KY + 1][MZ];
+#pragma unroll
+                        for (int kzi = 0; kzi < MZ; kzi++) {
+                            const cf w = c2(stage[(kzi >= KZ ? kzi - KZ : KZ - kzi) * 32 + lane]);
+                            v[0][kzi] = kzi >= KZ ? w : cconj(w);
+                        }
+#pragma unroll
+                        for (int ky = 1; ky <= KY; ky++)
+#pragma unroll
+                            for (int kzi = 0; kzi < MZ; kzi++)
+                                v[ky][kzi] = c2(stage[(G::spair(ky) + KX * MZ + kzi) * 32 + lane]);
+                        cf m[MZ];
+                        flip(m, v[1]);  // row -1
+                        cf t00 = tcol(m, v[0], v[1]);
+                        t00.i = 0.f;  // T(0,0) is real
+                        smooth(0, t00);
+#pragma unroll
+                        for (int ky = 1; ky <= KY; ky++) {
+                            if (ky == KY) flip(m, v[KY]);  // row KY + 1 == -KY
+                            smooth(G::tpair(ky) + KX, tcol(v[ky - 1], v[ky], ky < KY ? v[ky + 1] : m));
+                        }
+                    } else {
+                        // columns kx = +c (vp) and -c (vm); row 0 stores +c only:
+                        // C(0, -c, kz) = conj C(0, c, -kz)
+                        const float2 *pp = stage + (KX + c) * MZ * 32 + lane;
+                        const float2 *pm = stage + (KX - c) * MZ * 32 + lane;
+                        const float2 *p0 = stage + (KZ + 1 + (c - 1) * MZ) * 32 + lane;
+                        cf vp[KY + 1][MZ], vm[KY + 1][MZ];
+#pragma unroll
+                        for (int kzi = 0; kzi < MZ; kzi++) vp[0][kzi] = c2(p0[kzi * 32]);
+                        flip(vm[0], vp[0]);
+#pragma unroll
+                        for (int ky = 1; ky <= KY; ky++)
+#pragma unroll
+                            for (int kzi = 0; kzi < MZ; kzi++) {
+                                vp[ky][kzi] = c2(pp[(G::spair(ky) + kzi) * 32]);
+                                vm[ky][kzi] = c2(pm[(G::spair(ky) + kzi) * 32]);
+                            }
+                        cf m[MZ];
+                        flip(m, vm[1]);  // row -1 at +c
+                        smooth(c, tcol(m, vp[0], vp[1]));
+#pragma unroll
+                        for (int ky = 1; ky <= KY; ky++) {
+                            if (ky == KY) flip(m, vm[KY]);  // row KY + 1 at +c
+                            smooth(G::tpair(ky) + KX + c, tcol(vp[ky - 1], vp[ky], ky < KY ? vp[ky + 1] : m));
+                            if (ky == KY) flip(m, vp[KY]);  // row KY + 1 at -c
+                            smooth(G::tpair(ky) + KX - c, tcol(vm[ky - 1], vm[ky], ky < KY ? vm[ky + 1] : m));
+                        }
+                    }
                 }
             }
             if (CW_FENCE_ALL) fence_proxy_async();  // Hy reads of the stage before the next TMA write
