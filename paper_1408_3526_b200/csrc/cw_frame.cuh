@@ -32,6 +32,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace cwb {
 
 constexpr int MAXK = 5;    // largest half window supported by the tables
@@ -39,6 +41,9 @@ constexpr int MAXM = 2 * MAXK + 1;
 constexpr int MAXL = 33;   // largest lag grid per axis
 constexpr int LREC = (1 + 2 * MAXK + 3) / 4 * 4;  // floats per lag coefficient record
 constexpr int RESTART = 32;  // rows between direct y-SDFT restarts (bounds f32 drift)
+#ifndef CW_PREFETCH_LATE
+#define CW_PREFETCH_LATE 0  // issue the next-row / delayed-frame cp.async after barrier 2 instead of 1
+#endif
 #ifndef CW_FENCE_ALL
 #define CW_FENCE_ALL 1  // every thread orders its generic stage reads before the next TMA write
 #endif
@@ -625,12 +630,15 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                 continue;
             }
 
-            // async prefetches consumed in phases E (x stage of yy+1) and F (residual)
-            if (r == KY && yy + 1 < ye) prefetch_row(yy + 1, xb * 32);
-            if (r == 0) {
-                const size_t o = (size_t)(yy - a.mhy) * W + (x - a.mhx);
-                cp_async4(delbuf + lane, anchor ? a.delayed + o : a.frame, anchor);
-            }
+            // async prefetches consumed at the end of CD (x stage of yy+1) and in F (residual)
+            auto prefetch = [&]() {
+                if (r == KY && yy + 1 < ye) prefetch_row(yy + 1, xb * 32);
+                if (r == 0) {
+                    const size_t o = (size_t)(yy - a.mhy) * W + (x - a.mhx);
+                    cp_async4(delbuf + lane, anchor ? a.delayed + o : a.frame, anchor);
+                }
+            };
+            if (!CW_PREFETCH_LATE) prefetch();
             // ---------------- phase C1: Hy, power, kz collapse, smoothing ----------------
             // Column ownership (a transpose through shared memory): warp r owns
             // the spatial-frequency columns kx = +-c, c = r, r + NR, ..., over
@@ -727,6 +735,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
             __syncthreads();  // (2) T^ rows visible; the state stage is free
             CW_STAMP(6);  // barrier 2 wait
             if (yy + 1 < ye) issue(yy + 1, xb);
+            if (CW_PREFETCH_LATE) prefetch();
 
             // ---------------- phase CD: lag contraction + partial argmax ----------------
             // score(ly, lx) = gy gx R^(ly, lx); stage 1 along kx (B(ky, lx)) for
@@ -786,40 +795,122 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                         }
                     }
                 };
-                if (NL && t.sym_x) {
-                    // +-lx pairing: this warp owns |lx| = C0 + q for q = r, r + NR, ...
+                if (NL && t.sym_x && t.sym_y) {
+                    // Symmetric grids: lag column pairs C0 +- q, q = r + i NR, processed
+                    // JQ at a time (stage 1 shares the T^ loads and A/D sums, stage 2
+                    // the lag-table constants).  Columns are visited ly = 0, -1, +1,
+                    // -2, +2, ... (ascending rank within a column, |v|^2 grows with
+                    // |ly|, then iy ascending), so a strict '>' chain per column keeps
+                    // the reference's tie winner; for a +-ly pair, max(e - o, e + o)
+                    // = e + |o| (the same rounding), -ly on a tie (visited first).
                     constexpr int C0 = NL / 2;
-                    for (int q = r; q <= C0; q += NR) {
-                        const LagRec &L = t.s1v[C0 + q];
-                        const float g = L.gain;
-                        float bp0, bm0;
-                        cf bqp[KY + 1], bqm[KY + 1];  // B(ky, +-lx)
+                    constexpr int QPW = (C0 + NR) / NR;  // ceil((C0 + 1) / NR)
+                    auto group = [&](auto jq, int q0) {
+                        constexpr int JQ = decltype(jq)::value;
+                        int qs[JQ];
+                        float g[JQ];
+                        float2 cs[JQ][KX];
+#pragma unroll
+                        for (int j = 0; j < JQ; j++) {
+                            qs[j] = q0 + j * NR <= C0 ? q0 + j * NR : q0;  // past the grid: repeat q0
+                            const LagRec &L = t.s1v[C0 + qs[j]];
+                            g[j] = L.gain;
+#pragma unroll
+                            for (int kx = 0; kx < KX; kx++) cs[j][kx] = L.cs[kx];
+                        }
+                        // stage 1: B(ky, C0 +- q) for the JQ column pairs; column 2j is
+                        // +q, 2j+1 is -q (for q = 0 both are the centre column)
+                        float b0[2 * JQ];
+                        cf bq[2 * JQ][KY + 1];
                         {   // row 0: T(0,-kx) = conj T(0,kx):
                             // B(0, +-lx) = g T00 + 2 sum c Re T -+ 2 sum s Im T
-                            cf acc = cmk(0.f, 0.f);
+                            cf acc[JQ];
 #pragma unroll
-                            for (int kx = 1; kx <= KX; kx++) acc = cfma2(c2(L.cs[kx - 1]), tv(0, kx), acc);
-                            const float cp = fmaf(2.f, acc.r, g * tv(0, 0).r);
-                            bp0 = fmaf(2.f, acc.i, cp);
-                            bm0 = fmaf(-2.f, acc.i, cp);
+                            for (int j = 0; j < JQ; j++) acc[j] = cmk(0.f, 0.f);
+#pragma unroll
+                            for (int kx = 1; kx <= KX; kx++) {
+                                const cf tv0 = tv(0, kx);
+#pragma unroll
+                                for (int j = 0; j < JQ; j++) acc[j] = cfma2(c2(cs[j][kx - 1]), tv0, acc[j]);
+                            }
+                            const float t00 = tv(0, 0).r;
+#pragma unroll
+                            for (int j = 0; j < JQ; j++) {
+                                const float cp = fmaf(2.f, acc[j].r, g[j] * t00);
+                                b0[2 * j] = fmaf(2.f, acc[j].i, cp);
+                                b0[2 * j + 1] = fmaf(-2.f, acc[j].i, cp);
+                            }
                         }
 #pragma unroll
                         for (int ky = 1; ky <= KY; ky++) {
                             // P = (cr, ci) = g T0 + sum c A; Q = (sr, -si) = sum s (D.i, D.r)
-                            cf P = cmul2(cf{g, g}, tv(ky, 0)), Q = cmk(0.f, 0.f);
+                            cf P[JQ], Q[JQ];
+                            const cf t0 = tv(ky, 0);
+#pragma unroll
+                            for (int j = 0; j < JQ; j++) {
+                                P[j] = cmul2(cf{g[j], g[j]}, t0);
+                                Q[j] = cmk(0.f, 0.f);
+                            }
 #pragma unroll
                             for (int kx = 1; kx <= KX; kx++) {
                                 const cf tp = tv(ky, kx), tm = tv(ky, -kx);
                                 const cf A = cadd(tp, tm), D = csub(tp, tm);
-                                const float c = L.cs[kx - 1].x, sn = L.cs[kx - 1].y;
-                                P = cfma2(cf{c, c}, A, P);
-                                Q = cfma2(cf{sn, sn}, cf{D.i, D.r}, Q);
+#pragma unroll
+                                for (int j = 0; j < JQ; j++) {
+                                    const float c = cs[j][kx - 1].x, sn = cs[j][kx - 1].y;
+                                    P[j] = cfma2(cf{c, c}, A, P[j]);
+                                    Q[j] = cfma2(cf{sn, sn}, cf{D.i, D.r}, Q[j]);
+                                }
                             }
-                            bqp[ky] = cfma2(Q, cf{1.f, -1.f}, P);   // (cr + sr, ci + si)
-                            bqm[ky] = cfma2(Q, cf{-1.f, 1.f}, P);   // (cr - sr, ci - si)
+#pragma unroll
+                            for (int j = 0; j < JQ; j++) {
+                                bq[2 * j][ky] = cfma2(Q[j], cf{1.f, -1.f}, P[j]);      // (cr + sr, ci + si)
+                                bq[2 * j + 1][ky] = cfma2(Q[j], cf{-1.f, 1.f}, P[j]);  // (cr - sr, ci - si)
+                            }
                         }
-                        column(C0 + q, bp0, bqp);
-                        if (q) column(C0 - q, bm0, bqm);
+                        // stage 2 + in-column argmax, all 2 JQ columns per ly pair
+                        float cv[2 * JQ], co[2 * JQ];
+                        int cpi[2 * JQ];
+#pragma unroll
+                        for (int c = 0; c < 2 * JQ; c++) {
+                            float e = t.s2v[C0].gain * b0[c];
+#pragma unroll
+                            for (int k = 1; k <= KY; k++) e = fmaf(t.s2v[C0].cs[k - 1].x, bq[c][k].r, e);
+                            cv[c] = e;
+                            co[c] = 0.f;
+                            cpi[c] = 0;
+                        }
+#pragma unroll
+                        for (int pq = 1; pq <= C0; pq++) {
+                            const LagRec &L2 = t.s2v[C0 + pq];
+#pragma unroll
+                            for (int c = 0; c < 2 * JQ; c++) {
+                                // (e, o) = (g b0 + sum c Re B, sum s Im B); scores e -+ o
+                                cf eo = cmk(L2.gain * b0[c], 0.f);
+#pragma unroll
+                                for (int k = 1; k <= KY; k++) eo = cfma2(c2(L2.cs[k - 1]), bq[c][k], eo);
+                                const float m = eo.r + fabsf(eo.i);
+                                if (m > cv[c]) {
+                                    cv[c] = m;
+                                    cpi[c] = pq;
+                                    co[c] = eo.i;
+                                }
+                            }
+                        }
+#pragma unroll
+                        for (int c = 0; c < 2 * JQ; c++) {
+                            const int lx = (c & 1) ? C0 - qs[c >> 1] : C0 + qs[c >> 1];
+                            const int ci = co[c] > 0.f ? C0 + cpi[c] : C0 - cpi[c];
+                            const int rk = srank[ci * nlx + lx];
+                            if (better(cv[c], rk, best, brk)) { best = cv[c]; brk = rk; }
+                        }
+                    };
+                    constexpr int NG2 = QPW / 2;
+#pragma unroll
+                    for (int i = 0; i < NG2; i++) group(std::integral_constant<int, 2>{}, r + 2 * i * NR);
+                    if (QPW & 1) {
+                        const int q0 = r + (QPW - 1) * NR;
+                        if (q0 <= C0) group(std::integral_constant<int, 1>{}, q0);
                     }
                 } else {
                     for (int lx = r; lx < nlx; lx += NR) {
