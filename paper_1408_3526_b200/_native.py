@@ -49,13 +49,47 @@ class NativeError(RuntimeError):
     """A CUDA-side failure reported through the C ABI."""
 
 
-def build(verbose: bool = False) -> str:
-    """Compile csrc/cw_api.cu for sm_100a into libcw_b200.so (nvcc)."""
-    cmd = ["nvcc", *NVCC_FLAGS, "-o", LIB_PATH, os.path.join(CSRC, "cw_api.cu")]
+def instances(dev: bool = False):
+    """(KX, KY, KZ, BX, BY, NL) kernel instances, as csrc/cw_inst.cuh lists them."""
+    import re
+
+    if dev:
+        return [(4, 4, 2, 3, 3, 0), (4, 4, 2, 3, 3, 17)]
+    src = open(os.path.join(CSRC, "cw_inst.cuh")).read()
+    geos = re.findall(r"CW_INSTANCES_GEO\(X,\s*(\d+),\s*(\d+),\s*(\d+),\s*(\d+),\s*(\d+)\)", src)
+    return [tuple(int(v) for v in g) + (n,) for g in geos for n in (0, 9, 17, 33)]
+
+
+def build(verbose: bool = False, out: str | None = None, dev: bool = False, extra=()) -> str:
+    """Compile the C ABI (csrc/cw_api.cu) and every kernel instance
+    (csrc/cw_inst.cu, one translation unit per instance, in parallel) for
+    sm_100a and link them into libcw_b200.so (or ``out``)."""
+    import concurrent.futures as cf
+    import tempfile
+
+    out = out or LIB_PATH
+    base = [f for f in NVCC_FLAGS if f != "-shared"] + list(extra)
+    if dev:
+        base.append("-DCW_DEV_DEFAULT_ONLY")
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-    subprocess.run(cmd, check=True)
-    return LIB_PATH
+        base.append("-Xptxas=-v")
+    with tempfile.TemporaryDirectory(prefix="cw_build_") as tmp:
+        jobs = [["nvcc", *base, "-c", "-o", os.path.join(tmp, "cw_api.o"), os.path.join(CSRC, "cw_api.cu")]]
+        for inst in instances(dev):
+            defs = [f"-DCW_{k}={v}" for k, v in zip(("IKX", "IKY", "IKZ", "IBX", "IBY", "INL"), inst)]
+            obj = os.path.join(tmp, "cw_inst_" + "_".join(map(str, inst)) + ".o")
+            jobs.append(["nvcc", *base, *defs, "-c", "-o", obj, os.path.join(CSRC, "cw_inst.cu")])
+        with cf.ThreadPoolExecutor(max_workers=max(1, os.cpu_count() or 1)) as ex:
+            results = list(ex.map(lambda c: subprocess.run(c, capture_output=True, text=True), jobs))
+        for c, r in zip(jobs, results):
+            if verbose and r.stderr:
+                print(r.stderr)
+            if r.returncode != 0:
+                raise RuntimeError(f"nvcc failed: {' '.join(c)}\n{r.stderr}")
+        objs = [c[c.index("-o") + 1] for c in jobs]
+        subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out, *objs],
+                       check=True)
+    return out
 
 
 class cw_params(ctypes.Structure):

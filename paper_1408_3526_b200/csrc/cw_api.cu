@@ -6,8 +6,7 @@
 // launches one cw_frame_kernel per frame.  Reference counterparts are cited
 // per function; there is no CPU compute path: every frame runs on the GPU
 // or the call fails with CW_ERR_CUDA.
-#include "cw_frame.cuh"
-#include "cw_naive.cuh"
+#include "cw_inst.cuh"
 #include "../../include/cw_b200.h"
 
 #include <nvtx3/nvToolsExt.h>  // header-only NVTX ranges (visible in nsys / ncu --nvtx)
@@ -21,89 +20,47 @@
 
 using namespace cwb;
 
+// kernel instances, one translation unit each (cw_inst.cu)
+#define CW_DECLARE(a, b, c, d, e, n) LaunchFn CW_INST_FN(a, b, c, d, e, n)();
+CW_INSTANCES(CW_DECLARE)
+#undef CW_DECLARE
+
 namespace {
 
 thread_local std::string g_create_error;
 
-struct LaunchFn {
-    void (*launch)(const FrameArgs &, const Tables &, int grid, cudaStream_t);
-    void (*launch_naive)(const NaiveArgs &, const Tables &, int grid, cudaStream_t);
-    const void *naive_kernel;
-    size_t naive_smem;
-    const void *kernel;
-    int threads;
-    size_t smem;
-    int nsp, ntp, retp;  // float2 pairs per pixel: observer state, T^, retained
-    int nl;              // compiled lag count (0: runtime loops)
-};
-
-template <int KX, int KY, int KZ, int BX, int BY, int NL>
-void launch_inst(const FrameArgs &a, const Tables &t, int grid, cudaStream_t s)
-{
-    using G = Geo<KX, KY, KZ, BX, BY>;
-    cw_frame_kernel<G, NL><<<grid, G::NTHREADS, G::SMEM_BYTES, s>>>(a, t);
-}
-
-template <int KX, int KY, int KZ, int BX, int BY>
-void launch_naive_inst(const NaiveArgs &a, const Tables &t, int grid, cudaStream_t s)
-{
-    using G = Geo<KX, KY, KZ, BX, BY>;
-    constexpr size_t smem = sizeof(float) * (G::MZ * G::MY * (32 + G::MX - 1) + G::MZ * G::MY * G::XF * 32);
-    cw_naive_kernel<G><<<grid, G::NTHREADS, smem, s>>>(a, t);
-}
-
-template <int KX, int KY, int KZ, int BX, int BY, int NL>
-LaunchFn make_inst()
-{
-    using G = Geo<KX, KY, KZ, BX, BY>;
-    LaunchFn f;
-    f.launch = &launch_inst<KX, KY, KZ, BX, BY, NL>;
-    f.launch_naive = &launch_naive_inst<KX, KY, KZ, BX, BY>;
-    f.naive_kernel = reinterpret_cast<const void *>(&cw_naive_kernel<G>);
-    f.naive_smem = sizeof(float) * (G::MZ * G::MY * (32 + G::MX - 1) + G::MZ * G::MY * G::XF * 32);
-    f.kernel = reinterpret_cast<const void *>(&cw_frame_kernel<G, NL>);
-    f.threads = G::NTHREADS;
-    f.smem = G::SMEM_BYTES;
-    f.nsp = G::NSP;
-    f.ntp = G::NTP;
-    f.retp = G::RETP;
-    f.nl = NL;
-    return f;
-}
-
 // Compiled geometries: the default (4,4,2,3,3) and the SURVEY §8d C5 sweep.
 // Symmetric lag grids of 9/17/33 entries get fully unrolled contraction
-// kernels; any other grid runs the runtime-loop instance (NL = 0).
+// kernels; any other grid runs the runtime-loop instance (NL = 0), which
+// also carries the geometry's naive-spectrum kernel.  Each instance is its
+// own translation unit (cw_inst.cu, compiled once per CW_INSTANCES entry).
+
 bool find_inst(int kx, int ky, int kz, int bx, int by, int nl_sym, LaunchFn *out)
 {
-#define CW_GEO(a, b, c, d, e, ...)                                              \
-    if (kx == a && ky == b && kz == c && bx == d && by == e) {                 \
-        const int nls[] = {__VA_ARGS__};                                        \
-        (void)nls;                                                              \
-        CW_NLS(a, b, c, d, e)                                                   \
-        *out = make_inst<a, b, c, d, e, 0>();                                   \
-        return true;                                                            \
+    bool geo = false;
+    LaunchFn base{}, sym{};
+    bool have_sym = false;
+#define CW_FIND(a, b, c, d, e, n)                                   \
+    if (kx == a && ky == b && kz == c && bx == d && by == e) {      \
+        geo = true;                                                 \
+        if (n == 0) base = CW_INST_FN(a, b, c, d, e, n)();          \
+        else if (n == nl_sym) {                                     \
+            sym = CW_INST_FN(a, b, c, d, e, n)();                   \
+            have_sym = true;                                        \
+        }                                                           \
     }
-#ifdef CW_DEV_DEFAULT_ONLY
-#define CW_NLS(a, b, c, d, e) CW_NL(a, b, c, d, e, 17)
-#else
-#define CW_NLS(a, b, c, d, e) CW_NL(a, b, c, d, e, 9) CW_NL(a, b, c, d, e, 17) CW_NL(a, b, c, d, e, 33)
-#endif
-#define CW_NL(a, b, c, d, e, n)                                                 \
-    if (nl_sym == n) {                                                          \
-        *out = make_inst<a, b, c, d, e, n>();                                   \
-        return true;                                                            \
+    CW_INSTANCES(CW_FIND)
+#undef CW_FIND
+    if (!geo) return false;
+    if (have_sym) {  // the naive kernel lives in the NL = 0 unit
+        sym.launch_naive = base.launch_naive;
+        sym.naive_kernel = base.naive_kernel;
+        sym.naive_smem = base.naive_smem;
+        *out = sym;
+    } else {
+        *out = base;
     }
-    CW_GEO(4, 4, 2, 3, 3, 0)
-#ifndef CW_DEV_DEFAULT_ONLY  // dev builds (tools/dev_build.sh): default geometry, 17 lags only
-    CW_GEO(3, 3, 2, 2, 2, 0)
-    CW_GEO(5, 5, 2, 4, 4, 0)
-    CW_GEO(4, 4, 1, 3, 3, 0)
-#endif
-#undef CW_NLS
-#undef CW_NL
-#undef CW_GEO
-    return false;
+    return true;
 }
 
 }  // namespace

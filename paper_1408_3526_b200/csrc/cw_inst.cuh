@@ -1,0 +1,76 @@
+// cw_inst.cuh -- compiled kernel instances (geometry x lag count) and the
+// launch table the host side (cw_api.cu) dispatches through.
+#pragma once
+#include "cw_frame.cuh"
+#include "cw_naive.cuh"
+
+namespace cwb {
+
+struct LaunchFn {
+    void (*launch)(const FrameArgs &, const Tables &, int grid, cudaStream_t);
+    void (*launch_naive)(const NaiveArgs &, const Tables &, int grid, cudaStream_t);
+    const void *naive_kernel;
+    size_t naive_smem;
+    const void *kernel;
+    int threads;
+    size_t smem;
+    int nsp, ntp, retp;  // float2 pairs per pixel: observer state, T^, retained
+    int nl;              // compiled lag count (0: runtime loops)
+};
+
+// (KX, KY, KZ, BX, BY, NL): the default geometry and the SURVEY §8d C5 sweep;
+// NL = 9 / 17 / 33 are the fully unrolled symmetric-grid contractions.
+#ifdef CW_DEV_DEFAULT_ONLY  // dev builds (tools/dev_build.sh)
+#define CW_INSTANCES(X) X(4, 4, 2, 3, 3, 0) X(4, 4, 2, 3, 3, 17)
+#else
+#define CW_INSTANCES_GEO(X, a, b, c, d, e) X(a, b, c, d, e, 0) X(a, b, c, d, e, 9) X(a, b, c, d, e, 17) X(a, b, c, d, e, 33)
+#define CW_INSTANCES(X)                   \
+    CW_INSTANCES_GEO(X, 4, 4, 2, 3, 3)    \
+    CW_INSTANCES_GEO(X, 3, 3, 2, 2, 2)    \
+    CW_INSTANCES_GEO(X, 5, 5, 2, 4, 4)    \
+    CW_INSTANCES_GEO(X, 4, 4, 1, 3, 3)
+#endif
+#define CW_INST_FN(a, b, c, d, e, n) cw_inst_##a##_##b##_##c##_##d##_##e##_##n
+
+template <int KX, int KY, int KZ, int BX, int BY, int NL>
+void launch_inst(const FrameArgs &a, const Tables &t, int grid, cudaStream_t s)
+{
+    using G = Geo<KX, KY, KZ, BX, BY>;
+    cw_frame_kernel<G, NL><<<grid, G::NTHREADS, G::SMEM_BYTES, s>>>(a, t);
+}
+
+template <class G>
+constexpr size_t naive_smem_bytes()
+{
+    return sizeof(float) * (G::MZ * G::MY * (32 + G::MX - 1) + G::MZ * G::MY * G::XF * 32);
+}
+
+template <int KX, int KY, int KZ, int BX, int BY>
+void launch_naive_inst(const NaiveArgs &a, const Tables &t, int grid, cudaStream_t s)
+{
+    using G = Geo<KX, KY, KZ, BX, BY>;
+    cw_naive_kernel<G><<<grid, G::NTHREADS, naive_smem_bytes<G>(), s>>>(a, t);
+}
+
+template <int KX, int KY, int KZ, int BX, int BY, int NL>
+LaunchFn make_inst()
+{
+    using G = Geo<KX, KY, KZ, BX, BY>;
+    LaunchFn f{};
+    f.launch = &launch_inst<KX, KY, KZ, BX, BY, NL>;
+    if constexpr (NL == 0) {  // one naive kernel per geometry (in the NL = 0 unit)
+        f.launch_naive = &launch_naive_inst<KX, KY, KZ, BX, BY>;
+        f.naive_kernel = reinterpret_cast<const void *>(&cw_naive_kernel<G>);
+        f.naive_smem = naive_smem_bytes<G>();
+    }
+    f.kernel = reinterpret_cast<const void *>(&cw_frame_kernel<G, NL>);
+    f.threads = G::NTHREADS;
+    f.smem = G::SMEM_BYTES;
+    f.nsp = G::NSP;
+    f.ntp = G::NTP;
+    f.retp = G::RETP;
+    f.nl = NL;
+    return f;
+}
+
+}  // namespace cwb
