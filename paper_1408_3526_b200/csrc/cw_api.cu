@@ -28,6 +28,7 @@ CW_INSTANCES(CW_DECLARE)
 namespace {
 
 thread_local std::string g_create_error;
+void (*g_phase_clocks)(unsigned long long *) = nullptr;  // CW_PHASE_TIMING: the last created pipeline's unit
 
 // Compiled geometries: the default (4,4,2,3,3) and the SURVEY §8d C5 sweep.
 // Symmetric lag grids of 9/17/33 entries get fully unrolled contraction
@@ -403,6 +404,7 @@ int cw_create(const cw_params *p, int32_t width, int32_t height, int32_t device,
     h->lag_x.assign(p->lag_x, p->lag_x + p->n_lag_x);
     h->lag_y.assign(p->lag_y, p->lag_y + p->n_lag_y);
     h->fn = fn;
+    g_phase_clocks = fn.phase_clocks;
     build_tables(h);
     std::vector<float> coef;
     rc = build_coef(h, bank_c64, retained, n_retained, &coef);
@@ -877,10 +879,8 @@ int cw_detections(cw_handle *h, int64_t ticket, int32_t *n_total, float *xyr, in
 #ifdef CW_PHASE_TIMING
 extern "C" int cw_phase_clocks(unsigned long long *dst)  // [8][16], then zeroed
 {
-    cudaDeviceSynchronize();
-    cudaMemcpyFromSymbol(dst, cw_phase_clk, sizeof(unsigned long long) * 128);
-    static unsigned long long zero[128] = {};
-    cudaMemcpyToSymbol(cw_phase_clk, zero, sizeof zero);
+    if (!g_phase_clocks) return CW_ERR_VALUE;
+    g_phase_clocks(dst);
     return 0;
 }
 #endif

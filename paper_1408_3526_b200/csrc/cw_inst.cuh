@@ -16,7 +16,18 @@ struct LaunchFn {
     size_t smem;
     int nsp, ntp, retp;  // float2 pairs per pixel: observer state, T^, retained
     int nl;              // compiled lag count (0: runtime loops)
+    void (*phase_clocks)(unsigned long long *dst);  // CW_PHASE_TIMING builds: this unit's clocks
 };
+
+#ifdef CW_PHASE_TIMING
+inline void phase_clocks_read(unsigned long long *dst)  // [8][16], then zeroed
+{
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(dst, cw_phase_clk, sizeof(unsigned long long) * 128);
+    static unsigned long long zero[128] = {};
+    cudaMemcpyToSymbol(cw_phase_clk, zero, sizeof zero);
+}
+#endif
 
 // (KX, KY, KZ, BX, BY, NL): the default geometry and the SURVEY §8d C5 sweep;
 // NL = 9 / 17 / 33 are the fully unrolled symmetric-grid contractions.
@@ -70,6 +81,9 @@ LaunchFn make_inst()
     f.ntp = G::NTP;
     f.retp = G::RETP;
     f.nl = NL;
+#ifdef CW_PHASE_TIMING
+    f.phase_clocks = &phase_clocks_read;
+#endif
     return f;
 }
 
