@@ -300,11 +300,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase)
 #ifdef CW_PHASE_TIMING
 // per-warp clock64 accumulators (phase-timing builds only): [warp][event]
 __device__ unsigned long long cw_phase_clk[8][16];
-#define CW_STAMP(k)                                                                       \
-    do {                                                                                  \
-        const unsigned long long now = clock64();                                         \
-        clk_acc[k] += now - clk_prev;                                                     \
-        clk_prev = now;                                                                   \
+// the "memory" clobber pins each stamp between the surrounding barriers and
+// shared-memory accesses (a plain clock64() may be moved across them)
+__device__ __forceinline__ unsigned long long cw_clock_pinned()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t)::"memory");
+    return t;
+}
+#define CW_STAMP(k)                                   \
+    do {                                              \
+        const unsigned long long now = cw_clock_pinned(); \
+        clk_acc[k] += now - clk_prev;                 \
+        clk_prev = now;                               \
     } while (0)
 #else
 #define CW_STAMP(k) \
@@ -325,7 +333,7 @@ __global__ void __launch_bounds__(G::NTHREADS, G::MINB)
 cw_frame_kernel(const FrameArgs a, const Tables t)
 {
 #ifdef CW_PHASE_TIMING
-    unsigned long long clk_prev = clock64();
+    unsigned long long clk_prev = cw_clock_pinned();
     unsigned long long clk_acc[11] = {};
 #endif
     constexpr int KX = G::KX, KY = G::KY, KZ = G::KZ, BX = G::BX, BY = G::BY;

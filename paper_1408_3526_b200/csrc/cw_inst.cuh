@@ -20,7 +20,7 @@ struct LaunchFn {
 };
 
 #ifdef CW_PHASE_TIMING
-inline void phase_clocks_read(unsigned long long *dst)  // [8][16], then zeroed
+static void phase_clocks_read(unsigned long long *dst)  // [8][16], then zeroed
 {
     cudaDeviceSynchronize();
     cudaMemcpyFromSymbol(dst, cw_phase_clk, sizeof(unsigned long long) * 128);
