@@ -12,6 +12,8 @@ E = hdr.index("Instructions Executed")
 tot_s = tot_e = 0
 agg = []
 for r in rows[hdr_i + 1:]:
+    if r and r[0] == "File Path":  # next source file: stop (line numbers collide)
+        break
     if not r or not r[0].isdigit() or r[2] != "-":
         continue
     s, e = float(r[S] or 0), float(r[E] or 0)

@@ -29,6 +29,8 @@ S, E = hdr.index("Warp Stall Sampling (All Samples)"), hdr.index("Instructions E
 agg = {}
 fname = None
 for r in rows[hi + 1:]:
+    if r and r[0] == "File Path":  # next source file: stop (line numbers collide)
+        break
     if not r or not r[0].isdigit() or r[2] != "-":
         continue
     ln = int(r[0])

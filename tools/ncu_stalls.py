@@ -10,6 +10,8 @@ hdr = rows[hi]
 cols = {n: hdr.index(n) for n in reasons}
 tot = collections.Counter(); per = {n: collections.Counter() for n in reasons}; src = {}
 for r in rows[hi + 1:]:
+    if r and r[0] == "File Path":  # next source file: stop (line numbers collide)
+        break
     if not r or not r[0].isdigit() or r[2] != "-":
         continue
     ln = int(r[0]); src[ln] = r[1][:80]
