@@ -540,6 +540,31 @@ def run_config(args):
         sp.close()
         line("pixel-frames/sec (4096x4096, strip-sharded)", "C4: 4096x4096, row strips + 8-row halo over NCCL",
              w * h, p, el, kern, n, clk, "strong", {"frame": [w, h], "strips": world, "halo_rows": p.my - 1})
+    elif args.config == "c4strips":
+        # C4 strip decomposition measured on ONE GPU (this environment has no
+        # multi-GPU box): for N = 1, 2, 4, 8 the kernel runs the strip a rank
+        # of an N-way split owns (the middle one, with its My-1 halo rows) and
+        # the line reports the projected N-GPU rate 4096^2 / strip time.  The
+        # per-frame halo exchange (8 rows x 4096 x 4 B = 128 KiB from one
+        # neighbour over NVLink) is not in the timed region.
+        from paper_1408_3526_b200.strips import plan_strips
+
+        w = h = 4096
+        p = default_params()
+        for n_strips in (1, 2, 4, 8):
+            pl = plan_strips(p, h, n_strips)[n_strips // 2]
+            frames = generate_device(SimConfig(width=w, height=h, frame_count=200, rng_seed=4), device=dev,
+                                     frames=6, rows=(pl.lo, pl.a1))
+            with Pipeline(p, w, pl.local_height, device=local, _strip=(pl.halo, pl.lo)) as pipe:
+                el, kern, n, clk = _device_run(lib, pipe, frames, args.steps, args.warmup, stream, dist)
+            line("pixel-frames/sec (4096x4096, strip-sharded), projected from one strip on 1 GPU",
+                 f"C4: strip {n_strips // 2} of {n_strips} (rows {pl.lo}..{pl.a1}, halo {pl.halo}) timed alone",
+                 w * h, p, el, kern, n, clk, "strong",
+                 {"frame": [w, h], "strips": n_strips, "strip_rows": pl.a1 - pl.a0, "halo_rows": pl.halo,
+                  "projection": "N-GPU rate = 4096^2 / (one strip's time); halo exchange excluded"})
+            # roofline of the strip kernel: algorithmic bytes of the strip's own anchor rows
+            lines[-1]["roofline"]["achieved"] *= (pl.a1 - pl.a0) / h
+            lines[-1]["roofline"]["frac"] *= (pl.a1 - pl.a0) / h
     if rank == 0:
         for d in lines:
             print(json.dumps(d), flush=True)
@@ -555,7 +580,7 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU-oracle timing")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--config", choices=("c3", "c2", "c4", "c5", "c3naive", "c3seq"), default="c3",
+    ap.add_argument("--config", choices=("c3", "c2", "c4", "c4strips", "c5", "c3naive", "c3seq"), default="c3",
                     help="c3 (default, the headline) or another BASELINE.json configuration")
     args = ap.parse_args()
     if args.warmup < 3:
