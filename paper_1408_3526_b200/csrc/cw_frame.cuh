@@ -14,11 +14,15 @@
 //                 (_kernels.py:274-302)
 //   velocity-tuned PEF on the retained band + residual (_kernels.py:305-342)
 //
-// Work mapping (DESIGN.md §3): a CTA owns 32 adjacent columns (lane = pixel
-// column) and one warp per spatial-frequency row ky = 0..KY (real input =>
-// conjugate symmetry, only the half space is kept).  It walks a contiguous
-// run of the linearised (column-block, row) space, carrying the y-SDFT
-// resonator state in registers from row to row.
+// Work mapping (DESIGN.md §5): a CTA owns 32 adjacent columns (lane = pixel
+// column) and KY+1 warps (real input => conjugate symmetry, only the half
+// space is kept).  It walks a contiguous run of the linearised (column-block,
+// row) space, carrying the y-SDFT resonator state in registers from row to
+// row.  The owner of the work changes between phases: in the SDFT/observer
+// phase warp r owns spatial-frequency row ky = r (Hz, Hx in registers); in
+// the Hy/power/T^ phase it owns the columns kx = +-r over all rows (each Cx
+// value read once from shared memory); in the contraction it owns two lag
+// column pairs, processed jointly.
 //
 // Per-pixel state lives in HBM as "packets": for a (row, 32-column block),
 // the observer state is float2 P[pair][lane] (re/im pairs, lane-minor), so
