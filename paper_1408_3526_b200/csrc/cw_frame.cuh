@@ -48,6 +48,9 @@ constexpr int RESTART = 32;  // rows between direct y-SDFT restarts (bounds f32 
 #ifndef CW_PREFETCH_LATE
 #define CW_PREFETCH_LATE 0  // issue the next-row / delayed-frame cp.async after barrier 2 instead of 1
 #endif
+#ifndef CW_MEMONLY
+#define CW_MEMONLY 0  // diagnostic build: state / T^ / frame / output traffic only (tools: memory floor)
+#endif
 #ifndef CW_FENCE_ALL
 #define CW_FENCE_ALL 1  // every thread orders its generic stage reads before the next TMA write
 #endif
@@ -528,7 +531,10 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
             // z+ is exactly the reference's unnormalised temporal DFT of the
             // last Mz spatial spectra (_kernels.py:71-90, S = norm * z+).
             cf cz[MX][MZ];  // 4 x Hz(z+) per kx column
-            if (r == 0) {
+            if (CW_MEMONLY) {  // diagnostic: the same HBM traffic, no arithmetic
+                const int np = r == 0 ? G::ROW0P : G::ROWNP;
+                for (int j = 0; j < np; j++) stg[j * 32] = sst[j * 32];
+            } else if (r == 0) {
                 {   // DC spatial bin: real input; z(0) real, z(1..KZ) complex
                     const float uv = anchor ? sp[KX].r : 0.f;
                     cf zd[KZ + 1];
@@ -639,7 +645,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
             CW_STAMP(4);  // barrier 1 wait
             if (!a.ready) {
                 if (yy + 1 < ye) issue(yy + 1, xb);  // stage free: next row's state
-                continue;
+                    continue;
             }
 
             // async prefetches consumed at the end of CD (x stage of yy+1) and in F (residual)
@@ -688,7 +694,14 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
 #pragma unroll
                     for (int kzi = 0; kzi < MZ; kzi++) dst[kzi] = cconj(src[MZ - 1 - kzi]);
                 };
-                for (int c = r; c <= KX; c += NR) {
+                if (CW_MEMONLY) {
+                    const int np = r == 0 ? G::TROW0P : G::TROWNP;
+                    for (int j = 0; j < np; j++) {
+                        const float2 v = tstage[(G::tpair(r) + j) * 32 + lane];
+                        thg[(G::tpair(r) + j) * 32] = v;
+                    }
+                }
+                if (!CW_MEMONLY) for (int c = r; c <= KX; c += NR) {
                     if (c == 0) {
                         // column kx = 0: rows 0..KY; C(0, 0, -kz) = conj C(0, 0, kz)
                         cf v[KY + 1][MZ];
@@ -807,7 +820,10 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                         }
                     }
                 };
-                if (NL && t.sym_x && t.sym_y) {
+                if (CW_MEMONLY) {
+                    best = 0.f;
+                    brk = 0;
+                } else if (NL && t.sym_x && t.sym_y) {
                     // Symmetric grids: lag column pairs C0 +- q, q = r + i NR, processed
                     // JQ at a time (stage 1 shares the T^ loads and A/D sums, stage 2
                     // the lag-table constants).  Columns are visited ly = 0, -1, +1,
@@ -993,7 +1009,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                     viy = srxy[2 * brk + 1];
                 }
             }
-            if (r <= BY) {
+            if (!CW_MEMONLY && r <= BY) {
                 // PEF on the retained band (_kernels.py:330-342), folded to the
                 // stored half space: pred = sum_j coef[v][j] . z+[j]
                 const float2 *cp = a.coefP + (size_t)(viy * nlx + vix) * G::RETP + G::ppair(r);
