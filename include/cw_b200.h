@@ -82,6 +82,10 @@ int cw_set_forced_velocity(cw_handle *h, int32_t ix, int32_t iy);
  *  frame_index  : input index of the output frame (n - mhat_z)
  *  stream       : cudaStream_t to run on (NULL: the handle's own stream)
  * Synchronises `stream` before returning when any host output is given.
+ * When every given output buffer is page-locked host memory (cudaHostAlloc,
+ * torch pin_memory), the kernel writes the outputs into it directly while it
+ * runs (no device-to-host copies after the kernel); the residual/prediction
+ * border outside the valid region is zeroed on the host.
  */
 int cw_push(cw_handle *h, const float *frame, float *residual, float *prediction, uint8_t *vidx,
             int32_t *ready, int64_t *frame_index, void *stream);

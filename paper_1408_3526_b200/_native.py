@@ -60,7 +60,7 @@ def instances(dev: bool = False):
     return [tuple(int(v) for v in g) + (n,) for g in geos for n in (0, 9, 17, 33)]
 
 
-def build(verbose: bool = False, out: str | None = None, dev: bool = False, extra=()) -> str:
+def build(verbose: bool = False, out: str | None = None, dev: bool = False, extra=(), openmp: bool = True) -> str:
     """Compile the C ABI (csrc/cw_api.cu) and every kernel instance
     (csrc/cw_inst.cu, one translation unit per instance, in parallel) for
     sm_100a and link them into libcw_b200.so (or ``out``)."""
@@ -74,7 +74,8 @@ def build(verbose: bool = False, out: str | None = None, dev: bool = False, extr
     if verbose:
         base.append("-Xptxas=-v")
     with tempfile.TemporaryDirectory(prefix="cw_build_") as tmp:
-        jobs = [["nvcc", *base, "-c", "-o", os.path.join(tmp, "cw_api.o"), os.path.join(CSRC, "cw_api.cu")]]
+        omp = ["-Xcompiler", "-fopenmp"] if openmp else []
+        jobs = [["nvcc", *base, *omp, "-c", "-o", os.path.join(tmp, "cw_api.o"), os.path.join(CSRC, "cw_api.cu")]]
         for inst in instances(dev):
             defs = [f"-DCW_{k}={v}" for k, v in zip(("IKX", "IKY", "IKZ", "IBX", "IBY", "INL"), inst)]
             obj = os.path.join(tmp, "cw_inst_" + "_".join(map(str, inst)) + ".o")
@@ -87,7 +88,8 @@ def build(verbose: bool = False, out: str | None = None, dev: bool = False, extr
             if r.returncode != 0:
                 raise RuntimeError(f"nvcc failed: {' '.join(c)}\n{r.stderr}")
         objs = [c[c.index("-o") + 1] for c in jobs]
-        subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out, *objs],
+        subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out, *objs,
+                        *(["-lgomp"] if openmp else [])],
                        check=True)
     return out
 

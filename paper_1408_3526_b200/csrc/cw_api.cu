@@ -9,6 +9,9 @@
 #include "cw_inst.cuh"
 #include "../../include/cw_b200.h"
 
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 #include <nvtx3/nvToolsExt.h>  // header-only NVTX ranges (visible in nsys / ncu --nvtx)
 
 #include <algorithm>
@@ -98,6 +101,9 @@ struct cw_handle {
     int det_cap = 0;
     bool det_on = false;
     unsigned char *d_det = nullptr, *h_det = nullptr;
+    // pageable frames given to cw_push are staged here (pinned, multithreaded copy)
+    float *h_stage = nullptr;
+    cudaEvent_t ev_stage = nullptr;  // the last upload from h_stage
     size_t det_bytes = 0;
     size_t state_floats = 0, that_floats = 0;  // floats (pairs x 2)
     long long frames_seen = 0;
@@ -483,6 +489,12 @@ void cw_destroy(cw_handle *h)
     cudaFree(h->d_det);
     if (h->h_det)
         cudaFreeHost(h->h_det);
+    if (h->ev_stage) {
+        cudaEventSynchronize(h->ev_stage);
+        cudaEventDestroy(h->ev_stage);
+    }
+    if (h->h_stage)
+        cudaFreeHost(h->h_stage);
     for (cudaEvent_t e : h->ev_pool)
         cudaEventDestroy(e);
     for (int i = 0; i < cw_handle::NEV; i++) {
@@ -540,7 +552,11 @@ struct NvtxRange {
     ~NvtxRange() { nvtxRangePop(); }
 };
 
-static int run_frame(cw_handle *h, cudaStream_t s, int32_t *ready, int64_t *frame_index)
+// Outputs go to the handle's double-buffered device set unless res_o /
+// pred_o / vidx_o (device-addressable pointers, e.g. mapped host memory)
+// override them.
+static int run_frame(cw_handle *h, cudaStream_t s, int32_t *ready, int64_t *frame_index, float *res_o = nullptr,
+                     float *pred_o = nullptr, uint8_t *vidx_o = nullptr)
 {
     NvtxRange nvtx("cw_frame");
     const size_t HW = (size_t)h->W * h->H;
@@ -553,9 +569,9 @@ static int run_frame(cw_handle *h, cudaStream_t s, int32_t *ready, int64_t *fram
     a.that = reinterpret_cast<float2 *>(h->d_that);
     a.coefP = reinterpret_cast<const float2 *>(h->d_coef);
     const size_t set = (size_t)(n & 1);  // double-buffered outputs
-    a.res = h->d_res + set * HW;
-    a.pred = h->d_pred + set * HW;
-    a.vidx = h->d_vidx + set * HW * 2;
+    a.res = res_o ? res_o : h->d_res + set * HW;
+    a.pred = pred_o ? pred_o : h->d_pred + set * HW;
+    a.vidx = vidx_o ? vidx_o : h->d_vidx + set * HW * 2;
     a.W = h->W;
     a.H = h->H;
     a.NXB = h->NXB;
@@ -639,6 +655,20 @@ int cw_push_device(cw_handle *h, const float *frame_dev, int32_t *ready, int64_t
     return run_frame(h, s, ready, frame_index);
 }
 
+// Device address of page-locked host memory (UVA maps cudaHostAlloc /
+// torch pin_memory buffers at their host address), else nullptr.
+static void *mapped_host(const void *p)
+{
+    if (!p)
+        return nullptr;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
+}
+
 int cw_push(cw_handle *h, const float *frame, float *residual, float *prediction, uint8_t *vidx, int32_t *ready,
             int64_t *frame_index, void *stream)
 {
@@ -649,16 +679,78 @@ int cw_push(cw_handle *h, const float *frame, float *residual, float *prediction
     float *slot;
     cw_next_frame_slot(h, &slot);
     const size_t HW = (size_t)h->W * h->H;
-    CW_CUDA(h, cudaMemcpyAsync(slot, frame, HW * 4, cudaMemcpyHostToDevice, s));
+    const float *src = frame;
+    if (!mapped_host(frame)) {
+        // pageable frame: a parallel copy into a pinned staging buffer, then
+        // one DMA (the driver's own pageable path stages single-threaded)
+        if (!h->h_stage) {
+            CW_CUDA(h, cudaHostAlloc(reinterpret_cast<void **>(&h->h_stage), HW * 4, cudaHostAllocDefault));
+            CW_CUDA(h, cudaEventCreateWithFlags(&h->ev_stage, cudaEventDisableTiming));
+        } else {
+            CW_CUDA(h, cudaEventSynchronize(h->ev_stage));  // previous upload done with the buffer
+        }
+#ifdef _OPENMP
+        const int nt = std::max(1, std::min(8, omp_get_max_threads()));
+#else
+        const int nt = 1;
+#endif
+        const long long chunk = ((long long)HW + nt - 1) / nt;
+#pragma omp parallel for num_threads(nt) schedule(static)
+        for (int t = 0; t < nt; t++) {
+            const long long b = t * chunk, e = std::min((long long)HW, b + chunk);
+            if (b < e)
+                std::memcpy(h->h_stage + b, frame + b, sizeof(float) * (size_t)(e - b));
+        }
+        src = h->h_stage;
+    }
+    CW_CUDA(h, cudaMemcpyAsync(slot, src, HW * 4, cudaMemcpyHostToDevice, s));
+    if (src == h->h_stage)
+        CW_CUDA(h, cudaEventRecord(h->ev_stage, s));
     int32_t rd = 0;
     const size_t set = (size_t)(h->frames_seen & 1);
-    int rc = run_frame(h, s, &rd, frame_index);
+    const bool will_be_ready = h->frames_seen + 1 >= h->mz;
+    // Direct outputs: when every requested output buffer is page-locked host
+    // memory, the kernel writes residual / prediction / velocity straight
+    // into it over PCIe while it runs (10 B per pixel, far below the link
+    // rate), so no device-to-host copies follow the kernel.  The kernel
+    // writes the valid output rectangle and every velocity pair; the
+    // residual / prediction border outside valid_bounds (pipeline.py:41-50)
+    // is zeroed here on the host.  Full frames only (no strip halo).
+    float *res_d = nullptr, *pred_d = nullptr;
+    uint8_t *vidx_d = nullptr;
+    bool direct = will_be_ready && h->halo == 0 && h->row_off == 0 && (residual || prediction || vidx);
+    if (direct) {
+        res_d = static_cast<float *>(mapped_host(residual));
+        pred_d = static_cast<float *>(mapped_host(prediction));
+        vidx_d = static_cast<uint8_t *>(mapped_host(vidx));
+        direct = (!residual || res_d) && (!prediction || pred_d) && (!vidx || vidx_d);
+    }
+    if (direct) {
+        const int W = h->W, H = h->H;
+        const int x0 = h->mx - 1 - h->mhx, x1 = W - 1 - h->mhx, y0 = h->my - 1 - h->mhy, y1 = H - 1 - h->mhy;
+        for (float *o : {residual, prediction}) {
+            if (!o)
+                continue;
+            if (y0 > 0)
+                std::memset(o, 0, sizeof(float) * (size_t)y0 * W);
+            if (y1 + 1 < H)
+                std::memset(o + (size_t)(y1 + 1) * W, 0, sizeof(float) * (size_t)(H - 1 - y1) * W);
+            for (int y = std::max(y0, 0); y <= std::min(y1, H - 1); y++) {
+                float *row = o + (size_t)y * W;
+                if (x0 > 0)
+                    std::memset(row, 0, sizeof(float) * x0);
+                if (x1 + 1 < W)
+                    std::memset(row + x1 + 1, 0, sizeof(float) * (W - 1 - x1));
+            }
+        }
+    }
+    int rc = direct ? run_frame(h, s, &rd, frame_index, res_d, pred_d, vidx_d) : run_frame(h, s, &rd, frame_index);
     if (rc != CW_OK)
         return rc;
     if (ready)
         *ready = rd;
-    bool sync = false;
-    if (rd) {
+    bool sync = direct;
+    if (rd && !direct) {
         if (residual) {
             CW_CUDA(h, cudaMemcpyAsync(residual, h->d_res + set * HW, HW * 4, cudaMemcpyDeviceToHost, s));
             sync = true;

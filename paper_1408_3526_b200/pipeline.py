@@ -123,6 +123,26 @@ class _PinnedPool:
         weakref.finalize(arr, self._give, key, tensor)
         return arr
 
+    def take_outputs(self, h, w):
+        """(residual, prediction, velocity-index) arrays of one call, carved
+        from a single pinned block (one allocation / finalizer per call; the
+        block returns to the pool when the last of the three is collected)."""
+        import torch
+
+        key = ("outputs", h, w)
+        hw = h * w
+        with self._lock:
+            stack = self._free.setdefault(key, [])
+            tensor = stack.pop() if stack else None
+        if tensor is None:
+            tensor = torch.empty(10 * hw, dtype=torch.uint8, pin_memory=True)
+        blk = tensor.numpy()
+        weakref.finalize(blk, self._give, key, tensor)
+        res = blk[: 4 * hw].view(np.float32).reshape(h, w)
+        pred = blk[4 * hw : 8 * hw].view(np.float32).reshape(h, w)
+        vidx = blk[8 * hw :].reshape(h, w, 2)
+        return res, pred, vidx
+
     def _give(self, key, tensor):
         with self._lock:
             self._free.setdefault(key, []).append(tensor)
@@ -262,9 +282,7 @@ class Pipeline:
         lib = _native.load()
         t0 = time.perf_counter()
         h, w = self.height, self.width
-        res = self._pool.take((h, w), np.float32)
-        pred = self._pool.take((h, w), np.float32)
-        vidx = self._pool.take((h, w, 2), np.uint8)
+        res, pred, vidx = self._pool.take_outputs(h, w)
         ready = ctypes.c_int32(0)
         fidx = ctypes.c_int64(-1)
         rc = lib.cw_push(
@@ -321,9 +339,7 @@ class Pipeline:
             frame = np.ascontiguousarray(frame, dtype=">u2" if pgm else np.float32)
             if frame.shape != (h, w):
                 raise ValueError(f"frame shape {frame.shape} != {(h, w)}")
-            res = self._pool.take((h, w), np.float32)
-            pred = self._pool.take((h, w), np.float32)
-            vidx = self._pool.take((h, w, 2), np.uint8)
+            res, pred, vidx = self._pool.take_outputs(h, w)
             ticket = ctypes.c_int64(-1)
             rc = lib.cw_submit_raw(self._h, ctypes.c_void_p(frame.ctypes.data),
                                    _native.FMT_PGM16 if pgm else _native.FMT_F32LE, float(scale), float(offset),
