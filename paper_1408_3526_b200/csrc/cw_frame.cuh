@@ -45,9 +45,6 @@ constexpr int MAXM = 2 * MAXK + 1;
 constexpr int MAXL = 33;   // largest lag grid per axis
 constexpr int LREC = (1 + 2 * MAXK + 3) / 4 * 4;  // floats per lag coefficient record
 constexpr int RESTART = 32;  // rows between direct y-SDFT restarts (bounds f32 drift)
-#ifndef CW_PREFETCH_LATE
-#define CW_PREFETCH_LATE 0  // issue the next-row / delayed-frame cp.async after barrier 2 instead of 1
-#endif
 #ifndef CW_MEMONLY
 #define CW_MEMONLY 0  // diagnostic build: state / T^ / frame / output traffic only (tools: memory floor)
 #endif
@@ -649,14 +646,11 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
             }
 
             // async prefetches consumed at the end of CD (x stage of yy+1) and in F (residual)
-            auto prefetch = [&]() {
-                if (r == KY && yy + 1 < ye) prefetch_row(yy + 1, xb * 32);
-                if (r == 0) {
-                    const size_t o = (size_t)(yy - a.mhy) * W + (x - a.mhx);
-                    cp_async4(delbuf + lane, anchor ? a.delayed + o : a.frame, anchor);
-                }
-            };
-            if (!CW_PREFETCH_LATE) prefetch();
+            if (r == KY && yy + 1 < ye) prefetch_row(yy + 1, xb * 32);
+            if (r == 0) {
+                const size_t o = (size_t)(yy - a.mhy) * W + (x - a.mhx);
+                cp_async4(delbuf + lane, anchor ? a.delayed + o : a.frame, anchor);
+            }
             // ---------------- phase C1: Hy, power, kz collapse, smoothing ----------------
             // Column ownership (a transpose through shared memory): warp r owns
             // the spatial-frequency columns kx = +-c, c = r, r + NR, ..., over
@@ -760,7 +754,6 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
             __syncthreads();  // (2) T^ rows visible; the state stage is free
             CW_STAMP(6);  // barrier 2 wait
             if (yy + 1 < ye) issue(yy + 1, xb);
-            if (CW_PREFETCH_LATE) prefetch();
 
             // ---------------- phase CD: lag contraction + partial argmax ----------------
             // score(ly, lx) = gy gx R^(ly, lx); stage 1 along kx (B(ky, lx)) for
