@@ -983,8 +983,8 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
             if (yy + 1 < ye) issue_t(yy + 1, xb);
 
             // ---------------- phase E: final pick, PEF partials ----------------
-            int vix, viy;
-            {
+            int vix = 0, viy = 0;
+            if (r <= BY) {  // the PEF warps (warp 0 also stores the pair); warp KY goes straight on
                 const float2 bv = pbest[lane];
                 float best = bv.x;
                 int brk = __float_as_int(bv.y);
