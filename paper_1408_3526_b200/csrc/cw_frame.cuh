@@ -48,6 +48,9 @@ constexpr int RESTART = 32;  // rows between direct y-SDFT restarts (bounds f32 
 #ifndef CW_MEMONLY
 #define CW_MEMONLY 0  // diagnostic build: state / T^ / frame / output traffic only (tools: memory floor)
 #endif
+#ifndef CW_L2ONLY
+#define CW_L2ONLY 0  // diagnostic build: each CTA reuses one private packet (L2-resident state: the compute floor)
+#endif
 #ifndef CW_FENCE_ALL
 #define CW_FENCE_ALL 1  // every thread orders its generic stage reads before the next TMA write
 #endif
@@ -387,7 +390,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
     constexpr int ISSUER = G::NTHREADS - 32;  // lane 0 of warp KY: no PEF work, fewest lag columns
     auto issue = [&](int yy, int xb) {
         if (threadIdx.x == ISSUER) {
-            const size_t pix = (size_t)yy * NXB + xb;
+            const size_t pix = CW_L2ONLY ? (size_t)blockIdx.x : (size_t)yy * NXB + xb;
             fence_proxy_async();  // prior generic smem accesses before the async-proxy writes
             constexpr uint32_t bs = G::NSP * 32 * 8;
             mbar_expect_tx(bar, bs);
@@ -400,7 +403,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
     };
     auto issue_t = [&](int yy, int xb) {
         if (use_that && threadIdx.x == ISSUER) {
-            const size_t pix = (size_t)yy * NXB + xb;
+            const size_t pix = CW_L2ONLY ? (size_t)blockIdx.x : (size_t)yy * NXB + xb;
             fence_proxy_async();
             mbar_expect_tx(bar_t, G::SM_TSTAGE);
             tma_load(tstage, a.that + pix * G::NTP * 32, G::SM_TSTAGE, bar_t);
@@ -515,7 +518,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                 for (int i = 0; i < MX; i++) sp[i] = cadd(cmulw(sp[i], tw_r, twn_r), csub(xfv(s1, i - KX), xfv(s0, i - KX)));
             }
             const bool anchor = colv && x >= MX - 1 && (yy + a.y_off) >= MY - 1;
-            const size_t pix = (size_t)yy * NXB + xb;
+            const size_t pix = CW_L2ONLY ? (size_t)blockIdx.x : (size_t)yy * NXB + xb;
             float2 *stg = a.state + (pix * G::NSP + G::spair(r)) * 32 + lane;
             float2 *sst = stage + G::spair(r) * 32 + lane;
             CW_STAMP(1);  // x stage + y SDFT
