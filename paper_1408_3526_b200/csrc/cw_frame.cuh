@@ -51,6 +51,9 @@ constexpr int RESTART = 32;  // rows between direct y-SDFT restarts (bounds f32 
 #ifndef CW_L2ONLY
 #define CW_L2ONLY 0  // diagnostic build: each CTA reuses one private packet (L2-resident state: the compute floor)
 #endif
+#ifndef CW_ST_NA
+#define CW_ST_NA 1  // state / T^ stores with L1::no_allocate
+#endif
 #ifndef CW_FENCE_ALL
 #define CW_FENCE_ALL 1  // every thread orders its generic stage reads before the next TMA write
 #endif
@@ -327,6 +330,17 @@ __device__ __forceinline__ unsigned long long cw_clock_pinned()
     } while (0)
 #endif
 
+// state / T^ write-back: streaming stores that do not allocate in L1 (keep
+// the ~28 KB of L1 next to the shared memory for the PEF coefficients)
+__device__ __forceinline__ void st_state(float2 *p, float2 v)
+{
+#if CW_ST_NA
+    asm volatile("st.global.L1::no_allocate.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y));
+#else
+    *p = v;
+#endif
+}
+
 // 4-byte cp.async (LDGSTS) with zero fill when !valid (src-size 0)
 __device__ __forceinline__ void cp_async4(void *dst, const float *src, bool valid)
 {
@@ -533,7 +547,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
             cf cz[MX][MZ];  // 4 x Hz(z+) per kx column
             if (CW_MEMONLY) {  // diagnostic: the same HBM traffic, no arithmetic
                 const int np = r == 0 ? G::ROW0P : G::ROWNP;
-                for (int j = 0; j < np; j++) stg[j * 32] = sst[j * 32];
+                for (int j = 0; j < np; j++) st_state(&stg[j * 32], sst[j * 32]);
             } else if (r == 0) {
                 {   // DC spatial bin: real input; z(0) real, z(1..KZ) complex
                     const float uv = anchor ? sp[KX].r : 0.f;
@@ -545,12 +559,12 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                     for (int kz = 1; kz <= KZ; kz++) sum = fmaf(2.f, zd[kz].r, sum);
                     const float e = fmaf(-t.inv_mz, sum, uv);
                     const float z0 = zd[0].r + e;
-                    stg[0] = make_float2(z0, 0.f);
+                    st_state(&stg[0], make_float2(z0, 0.f));
                     sret[lane] = make_float2(z0, 0.f);
 #pragma unroll
                     for (int kz = 1; kz <= KZ; kz++) {
                         const cf zp = cmk(zd[kz].r + e, zd[kz].i);
-                        stg[kz * 32] = f2(cmulw(zp, t.w2[kz + KZ], t.wn2[kz + KZ]));
+                        st_state(&stg[kz * 32], f2(cmulw(zp, t.w2[kz + KZ], t.wn2[kz + KZ])));
                         sret[kz * 32 + lane] = f2(zp);
                     }
                 }
@@ -574,7 +588,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                     for (int kzi = 0; kzi < MZ; kzi++) {
                         zp[kzi] = cadd(z[kzi], e);
                         const cf zn = (kzi == KZ) ? zp[kzi] : cmulw(zp[kzi], t.w2[kzi], t.wn2[kzi]);
-                        stg[(base + kzi) * 32] = f2(zn);
+                        st_state(&stg[(base + kzi) * 32], f2(zn));
                         if (kx <= BX) sret[(base + kzi) * 32 + lane] = f2(zp[kzi]);
                     }
 #pragma unroll
@@ -621,7 +635,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                     for (int kzi = 0; kzi < MZ; kzi++) {
                         zp[kzi] = cadd(z[kzi], e);
                         const cf zn = (kzi == KZ) ? zp[kzi] : cmulw(zp[kzi], t.w2[kzi], t.wn2[kzi]);
-                        stg[(kxi * MZ + kzi) * 32] = f2(zn);
+                        st_state(&stg[(kxi * MZ + kzi) * 32], f2(zn));
                         if (r <= BY && kxb >= 0 && kxb < G::WX) rr[(kxb * MZ + kzi) * 32] = f2(zp[kzi]);
                     }
 #pragma unroll
@@ -672,7 +686,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                         const float2 o = tstage[j * 32 + lane];
                         v2 = cfma2(cf{t.beta, t.beta}, v2, cmul2(cf{t.alpha, t.alpha}, c2(o)));
                     }
-                    thg[j * 32] = f2(v2);
+                    st_state(&thg[j * 32], f2(v2));
                     tstage[j * 32 + lane] = f2(v2);
                 };
                 // 4^3 x the Hann-conditioned power, collapsed over kz with a_z
@@ -695,7 +709,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                     const int np = r == 0 ? G::TROW0P : G::TROWNP;
                     for (int j = 0; j < np; j++) {
                         const float2 v = tstage[(G::tpair(r) + j) * 32 + lane];
-                        thg[(G::tpair(r) + j) * 32] = v;
+                        st_state(&thg[(G::tpair(r) + j) * 32], v);
                     }
                 }
                 if (!CW_MEMONLY) for (int c = r; c <= KX; c += NR) {
