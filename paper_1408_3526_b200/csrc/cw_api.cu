@@ -298,7 +298,11 @@ static int build_coef(cw_handle *h, const float *bank, const int64_t *retained, 
     // float2 pairs per velocity, in the kernel's retained z+ order:
     // row 0: DC (kz = 0 real + zero pad, kz = 1..KZ), kx = 1..BX (all kz);
     // rows ky = 1..BY: kx = -BX..BX (all kz)
-    const int NRET = 2 * ((KZ + 1) + BX * Mz + BY * WX * Mz);
+    // rows padded to even pair counts (zero pad pairs) for the kernel's
+    // 16-byte two-pair loads (Geo::RETPP)
+    const int P0 = (KZ + 1) + BX * Mz, PN = WX * Mz;
+    const int P0p = (P0 + 1) / 2 * 2, PNp = (PN + 1) / 2 * 2;
+    const int NRET = 2 * (P0p + BY * PNp);
     out->assign((size_t)h->nlx * h->nly * NRET, 0.f);
     for (int v = 0; v < h->nlx * h->nly; v++) {
         const float *bk = bank + (size_t)v * nret * 2;
@@ -333,11 +337,14 @@ static int build_coef(cw_handle *h, const float *bank, const int64_t *retained, 
             for (int kz = -KZ; kz <= KZ; kz++)
                 if (!pair(kz, 0, kx))
                     return CW_ERR_VALUE;
-        for (int ky = 1; ky <= BY; ky++)
+        w = 2 * P0p;  // pad pair stays zero
+        for (int ky = 1; ky <= BY; ky++) {
             for (int kx = -BX; kx <= BX; kx++)
                 for (int kz = -KZ; kz <= KZ; kz++)
                     if (!pair(kz, ky, kx))
                         return CW_ERR_VALUE;
+            w = 2 * (P0p + ky * PNp);
+        }
         if (w != NRET)
             return CW_ERR_VALUE;
     }
@@ -417,6 +424,10 @@ int cw_create(const cw_params *p, int32_t width, int32_t height, int32_t device,
     if (rc != CW_OK) {
         delete h;
         return fail(nullptr, rc, "bank/retained layout inconsistent with the parameters");
+    }
+    if (coef.size() != (size_t)h->nlx * h->nly * 2 * fn.retp) {  // host layout == kernel's padded rows
+        delete h;
+        return fail(nullptr, CW_ERR_UNSUPPORTED, "PEF coefficient layout does not match the kernel instance");
     }
 
     auto cleanup_fail = [&](int code, const std::string &m) {

@@ -103,7 +103,7 @@ struct FrameArgs {
     const float *delayed;  // (H, W) frame n - mhat_z (nullptr until ready)
     float2 *state;         // observer state packets [H*NXB][NSP][32]
     float2 *that;          // smoothing state T^ packets [H*NXB][NTP][32]
-    const float2 *coefP;   // PEF coefficients [Ly*Lx][RETP]
+    const float2 *coefP;   // PEF coefficients [Ly*Lx][RETPP] (rows padded to even pair counts)
     float *res;            // (H, W) residual out
     float *pred;           // (H, W) prediction out (nullable)
     uint8_t *vidx;         // (H, W, 2) velocity index out
@@ -172,15 +172,20 @@ struct Geo {
     // retained z+ pairs (== PEF coefficient pairs)
     static constexpr int PROW0P = (KZ + 1) + BX * MZ, PROWNP = WX * MZ;
     static constexpr int RETP = PROW0P + BY * PROWNP;
+    // the same rows padded to even pair counts: 16-byte (2-pair) coefficient
+    // loads and (re, im, re, im) retained-z+ quads in shared memory
+    static constexpr int PROW0Q = (PROW0P + 1) / 2, PROWNQ = (PROWNP + 1) / 2;  // quads per row
+    static constexpr int RETPP = 2 * (PROW0Q + BY * PROWNQ);                    // padded pairs
     static constexpr int RING = MY + 2;           // x-stage ring rows
     static constexpr int XF = MX;                 // x-stage floats per (row, col)
     __host__ __device__ static constexpr int spair(int r) { return r == 0 ? 0 : ROW0P + (r - 1) * ROWNP; }
     __host__ __device__ static constexpr int tpair(int r) { return r == 0 ? 0 : TROW0P + (r - 1) * TROWNP; }
     __host__ __device__ static constexpr int ppair(int r) { return r == 0 ? 0 : PROW0P + (r - 1) * PROWNP; }
+    __host__ __device__ static constexpr int pquad(int r) { return r == 0 ? 0 : PROW0Q + (r - 1) * PROWNQ; }
     // shared memory plan (bytes)
     static constexpr int SM_STAGE = NSP * 32 * 8;     // state packet -> Cx in place
     static constexpr int SM_TSTAGE = NTP * 32 * 8;    // T^ packet
-    static constexpr int SM_RET = RETP * 32 * 8;      // retained z+
+    static constexpr int SM_RET = RETPP * 32 * 8;     // retained z+ quads
     static constexpr int SM_XF = RING * XF * 32 * 4;  // x-stage ring
     static constexpr int SM_BEST = NR * 32 * 8;       // partial argmax (score, rank)
     static constexpr int SM_PEF = (BY + 1) * 32 * 4;
@@ -341,6 +346,8 @@ __device__ __forceinline__ void st_state(float2 *p, float2 v)
 #endif
 }
 
+__device__ __forceinline__ float4 ldg_coef4(const float4 *p) { return __ldg(p); }
+
 // 4-byte cp.async (LDGSTS) with zero fill when !valid (src-size 0)
 __device__ __forceinline__ void cp_async4(void *dst, const float *src, bool valid)
 {
@@ -364,7 +371,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     float2 *stage = reinterpret_cast<float2 *>(smem_raw);                       // [NSP][32]
     float2 *tstage = reinterpret_cast<float2 *>(smem_raw + G::SM_STAGE);        // [NTP][32]
-    float2 *sret = reinterpret_cast<float2 *>(smem_raw + G::SM_STAGE + G::SM_TSTAGE);  // [RETP][32]
+    float2 *sret = reinterpret_cast<float2 *>(smem_raw + G::SM_STAGE + G::SM_TSTAGE);  // [RETPP][32]
     float *xfr = reinterpret_cast<float *>(smem_raw + G::SM_STAGE + G::SM_TSTAGE + G::SM_RET);
     float2 *pbest = reinterpret_cast<float2 *>(smem_raw + G::SM_STAGE + G::SM_TSTAGE + G::SM_RET + G::SM_XF);
     float *ppef = reinterpret_cast<float *>(reinterpret_cast<unsigned char *>(pbest) + G::SM_BEST);
@@ -544,6 +551,8 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
             //   e = u - (1/Mz) sum_kz z ;  z+ = z + e ;  z <- w(kz) z+
             // z+ is exactly the reference's unnormalised temporal DFT of the
             // last Mz spatial spectra (_kernels.py:71-90, S = norm * z+).
+            // retained z+ (the PEF input), pair q of the padded layout
+            auto rput = [&](int q, cf v) { sret[q * 32 + lane] = f2(v); };
             cf cz[MX][MZ];  // 4 x Hz(z+) per kx column
             if (CW_MEMONLY) {  // diagnostic: the same HBM traffic, no arithmetic
                 const int np = r == 0 ? G::ROW0P : G::ROWNP;
@@ -560,12 +569,12 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                     const float e = fmaf(-t.inv_mz, sum, uv);
                     const float z0 = zd[0].r + e;
                     st_state(&stg[0], make_float2(z0, 0.f));
-                    sret[lane] = make_float2(z0, 0.f);
+                    rput(0, cmk(z0, 0.f));
 #pragma unroll
                     for (int kz = 1; kz <= KZ; kz++) {
                         const cf zp = cmk(zd[kz].r + e, zd[kz].i);
                         st_state(&stg[kz * 32], f2(cmulw(zp, t.w2[kz + KZ], t.wn2[kz + KZ])));
-                        sret[kz * 32 + lane] = f2(zp);
+                        rput(kz, zp);
                     }
                 }
                 // DC suppression (_kernels.py:167-174): C(kz, 0, 0) = 0
@@ -589,12 +598,13 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                         zp[kzi] = cadd(z[kzi], e);
                         const cf zn = (kzi == KZ) ? zp[kzi] : cmulw(zp[kzi], t.w2[kzi], t.wn2[kzi]);
                         st_state(&stg[(base + kzi) * 32], f2(zn));
-                        if (kx <= BX) sret[(base + kzi) * 32 + lane] = f2(zp[kzi]);
+                        if (kx <= BX) rput(base + kzi, zp[kzi]);
                     }
 #pragma unroll
                     for (int kzi = 0; kzi < MZ; kzi++)
                         cz[KX + kx][kzi] = hann4(zp[(kzi + MZ - 1) % MZ], zp[kzi], zp[(kzi + 1) % MZ]);
                 }
+                if (G::PROW0P & 1) rput(G::PROW0P, cmk(0.f, 0.f));  // pad pair (zero coefficient)
                 // kx < 0 by symmetry: C(kz, 0, -kx) = conj C(-kz, 0, kx)
 #pragma unroll
                 for (int kx = 1; kx <= KX; kx++)
@@ -617,7 +627,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                         }
                 }
             } else {
-                float2 *rr = sret + G::ppair(r <= BY ? r : 0) * 32 + lane;
+                const int rq = G::pquad(r <= BY ? r : 0);  // this row's first retained quad
 #pragma unroll
                 for (int kxi = 0; kxi < MX; kxi++) {
                     const cf uv = anchor ? sp[kxi] : cmk(0.f, 0.f);
@@ -636,12 +646,13 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                         zp[kzi] = cadd(z[kzi], e);
                         const cf zn = (kzi == KZ) ? zp[kzi] : cmulw(zp[kzi], t.w2[kzi], t.wn2[kzi]);
                         st_state(&stg[(kxi * MZ + kzi) * 32], f2(zn));
-                        if (r <= BY && kxb >= 0 && kxb < G::WX) rr[(kxb * MZ + kzi) * 32] = f2(zp[kzi]);
+                        if (r <= BY && kxb >= 0 && kxb < G::WX) rput(2 * rq + kxb * MZ + kzi, zp[kzi]);
                     }
 #pragma unroll
                     for (int kzi = 0; kzi < MZ; kzi++)
                         cz[kxi][kzi] = hann4(zp[(kzi + MZ - 1) % MZ], zp[kzi], zp[(kzi + 1) % MZ]);
                 }
+                if (r <= BY && (G::PROWNP & 1)) rput(2 * rq + G::PROWNP, cmk(0.f, 0.f));  // pad pair
                 if (a.ready) {
                     // Hx (circular along kx), in place over this row's staged state
 #pragma unroll
@@ -1021,22 +1032,24 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
             }
             if (!CW_MEMONLY && r <= BY) {
                 // PEF on the retained band (_kernels.py:330-342), folded to the
-                // stored half space: pred = sum_j coef[v][j] . z+[j]
-                const float2 *cp = a.coefP + (size_t)(viy * nlx + vix) * G::RETP + G::ppair(r);
-                const float2 *sr = sret + G::ppair(r) * 32 + lane;
+                // stored half space: pred = sum_j coef[v][j] . z+[j], two pairs
+                // (one 16-byte coefficient load, one retained quad) per step
+                const float4 *cp = reinterpret_cast<const float4 *>(a.coefP + (size_t)(viy * nlx + vix) * G::RETPP) +
+                                   G::pquad(r);
+                const float2 *sr = sret + 2 * G::pquad(r) * 32 + lane;
                 cf acc[2] = {cmk(0.f, 0.f), cmk(0.f, 0.f)};  // packed (c.x z.x, c.y z.y) partial sums
+                auto quad = [&](int k) {
+                    const float4 c = ldg_coef4(cp + k);
+                    const float2 z0 = sr[(2 * k) * 32], z1 = sr[(2 * k + 1) * 32];
+                    acc[0] = cfma2(cmk(c.x, c.y), c2(z0), acc[0]);
+                    acc[1] = cfma2(cmk(c.z, c.w), c2(z1), acc[1]);
+                };
                 if (r == 0) {
 #pragma unroll
-                    for (int j = 0; j < G::PROW0P; j++) {
-                        const float2 c = __ldg(cp + j), z = sr[j * 32];
-                        acc[j & 1] = cfma2(c2(c), c2(z), acc[j & 1]);
-                    }
+                    for (int k = 0; k < G::PROW0Q; k++) quad(k);
                 } else {
 #pragma unroll
-                    for (int j = 0; j < G::PROWNP; j++) {
-                        const float2 c = __ldg(cp + j), z = sr[j * 32];
-                        acc[j & 1] = cfma2(c2(c), c2(z), acc[j & 1]);
-                    }
+                    for (int k = 0; k < G::PROWNQ; k++) quad(k);
                 }
                 const cf sum = cadd(acc[0], acc[1]);
                 ppef[r * 32 + lane] = sum.r + sum.i;

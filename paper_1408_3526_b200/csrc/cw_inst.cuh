@@ -14,7 +14,7 @@ struct LaunchFn {
     const void *kernel;
     int threads;
     size_t smem;
-    int nsp, ntp, retp;  // float2 pairs per pixel: observer state, T^, retained
+    int nsp, ntp, retp;  // float2 pairs per pixel: observer state, T^, retained (PEF rows padded)
     int nl;              // compiled lag count (0: runtime loops)
     void (*phase_clocks)(unsigned long long *dst);  // CW_PHASE_TIMING builds: this unit's clocks
 };
@@ -79,7 +79,7 @@ LaunchFn make_inst()
     f.smem = G::SMEM_BYTES;
     f.nsp = G::NSP;
     f.ntp = G::NTP;
-    f.retp = G::RETP;
+    f.retp = G::RETPP;
     f.nl = NL;
 #ifdef CW_PHASE_TIMING
     f.phase_clocks = &phase_clocks_read;
