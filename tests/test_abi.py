@@ -70,3 +70,24 @@ def test_create_rejects_bad_geometry_before_cuda(params, default_bank):
     rc = lib.cw_create(ctypes.byref(cp), 64, 64, 0, _native.fptr(coeffs.view(np.float32)),
                        ret.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), ret.size - 1, 0, 0, ctypes.byref(h))
     assert rc == _native.CW_ERR_VALUE
+
+
+def test_compiled_instances_cover_the_benchmarked_geometries():
+    """Every geometry bench.py measures (default, the SURVEY §8d C5 sweep)
+    has a compiled kernel instance, with the unrolled 9/17/33-lag
+    contractions and the runtime-loop fallback, each in the library."""
+    import bench
+
+    from paper_1408_3526_b200 import FilterParams, default_params
+
+    inst = set(_native.instances())
+    for kw in [dict(), *bench.C5_SWEEP.values()]:
+        p = FilterParams(**kw) if kw else default_params()
+        geo = (p.kx, p.ky, p.kz, p.bx, p.by)
+        assert geo + (0,) in inst, geo
+        n = len(p.lag_grid_x)
+        if n == len(p.lag_grid_y) and n in (9, 17, 33):
+            assert geo + (n,) in inst, (geo, n)
+    out = subprocess.run(["cuobjdump", "-sass", _native.LIB_PATH], capture_output=True, text=True).stdout
+    kernels = set(re.findall(r"Function : (_ZN3cwb15cw_frame_kernel\S+)", out))
+    assert len(kernels) == len(inst)
