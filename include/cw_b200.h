@@ -81,7 +81,9 @@ int cw_set_forced_velocity(cw_handle *h, int32_t ix, int32_t iy);
  *  ready        : 1 when an output frame was produced (frames_seen >= Mz)
  *  frame_index  : input index of the output frame (n - mhat_z)
  *  stream       : cudaStream_t to run on (NULL: the handle's own stream)
- * Synchronises `stream` before returning when any host output is given.
+ * Synchronises `stream` before returning when any host output is given or
+ * when `frame` is page-locked (pageable frames are staged before the call
+ * returns), so the caller may reuse every buffer afterwards.
  * When every given output buffer is page-locked host memory (cudaHostAlloc,
  * torch pin_memory), the kernel writes the outputs into it directly while it
  * runs (no device-to-host copies after the kernel); the residual/prediction

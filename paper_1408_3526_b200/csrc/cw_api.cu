@@ -760,7 +760,10 @@ int cw_push(cw_handle *h, const float *frame, float *residual, float *prediction
         return rc;
     if (ready)
         *ready = rd;
-    bool sync = direct;
+    // return only once the caller's buffers are no longer read or written:
+    // host outputs given (as documented), or a page-locked input frame whose
+    // upload is still in flight (a pageable one was staged synchronously)
+    bool sync = direct || residual || prediction || vidx || src != h->h_stage;
     if (rd && !direct) {
         if (residual) {
             CW_CUDA(h, cudaMemcpyAsync(residual, h->d_res + set * HW, HW * 4, cudaMemcpyDeviceToHost, s));
