@@ -127,8 +127,9 @@ def load():
         "cw_destroy": (None, [vp]),
         "cw_last_error": (ctypes.c_char_p, [vp]),
         "cw_set_forced_velocity": (ctypes.c_int, [vp, i32, i32]),
-        "cw_push": (ctypes.c_int, [vp, P(ctypes.c_float), P(ctypes.c_float), P(ctypes.c_float),
-                                   P(ctypes.c_uint8), P(i32), P(i64), vp]),
+        # buffer arguments as void*: the per-frame call passes raw addresses
+        # (ndarray.ctypes.data), which is cheaper than building typed pointers
+        "cw_push": (ctypes.c_int, [vp, vp, vp, vp, vp, P(i32), P(i64), vp]),
         "cw_push_device": (ctypes.c_int, [vp, vp, P(i32), P(i64), vp]),
         "cw_device_outputs": (ctypes.c_int, [vp, P(vp), P(vp), P(vp)]),
         "cw_next_frame_slot": (ctypes.c_int, [vp, P(vp)]),

@@ -285,11 +285,8 @@ class Pipeline:
         res, pred, vidx = self._pool.take_outputs(h, w)
         ready = ctypes.c_int32(0)
         fidx = ctypes.c_int64(-1)
-        rc = lib.cw_push(
-            self._h, _native.fptr(frame), _native.fptr(res), _native.fptr(pred),
-            vidx.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)),
-            ctypes.byref(ready), ctypes.byref(fidx), None,
-        )
+        rc = lib.cw_push(self._h, frame.ctypes.data, res.ctypes.data, pred.ctypes.data, vidx.ctypes.data,
+                         ctypes.byref(ready), ctypes.byref(fidx), None)
         _native.check(rc, self._h)
         self.last_timings = {"pipeline": time.perf_counter() - t0}
         if self._device_timing:
