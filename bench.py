@@ -308,18 +308,25 @@ def run_ours(args):
         for i in range(sync_steps):
             out_sync = pub.process_frame(host_np[i % n_host])
         sync_s = time.perf_counter() - t0
+        # ... and with ordinary (pageable) numpy frames, as a reference user passes them
+        page_np = host_np[: min(n_host, 16)].copy()
+        t0 = time.perf_counter()
+        for i in range(sync_steps):
+            out_sync = pub.process_frame(page_np[i % page_np.shape[0]])
+        sync_page_s = time.perf_counter() - t0
     assert n_out == e2e_steps and out_sync is not None
     h2d = WIDTH * HEIGHT * 4
     d2h = WIDTH * HEIGHT * (4 + 4 + 2)
 
-    t = torch.tensor([elapsed_ms, e2e_s, sync_s], dtype=torch.float64, device=dev)
+    t = torch.tensor([elapsed_ms, e2e_s, sync_s, sync_page_s], dtype=torch.float64, device=dev)
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    elapsed_ms, e2e_s, sync_s = float(t[0]), float(t[1]), float(t[2])
+    elapsed_ms, e2e_s, sync_s, sync_page_s = (float(v) for v in t)
     px = WIDTH * HEIGHT
     value = world * px * args.steps / (elapsed_ms / 1e3)
     e2e = world * px * e2e_steps / e2e_s
     e2e_sync = world * px * sync_steps / sync_s
+    e2e_sync_page = world * px * sync_steps / sync_page_s
 
     peak, peak_kind = measured_peak()
     bpp = b_alg(p, with_prediction=True)
@@ -351,7 +358,10 @@ def run_ours(args):
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "api": "Pipeline.process_stream (pinned host frames in; host residual, prediction, "
                            "velocity pairs out per step; depth-3 pipelining)",
-                    "sync_process_frame": {"value": e2e_sync, "unit": UNIT, "steps": sync_steps}},
+                    "sync_process_frame": {"value": e2e_sync, "unit": UNIT, "steps": sync_steps,
+                                           "frames": "pinned"},
+                    "sync_process_frame_pageable": {"value": e2e_sync_page, "unit": UNIT, "steps": sync_steps,
+                                                    "frames": "pageable numpy"}},
             "gpu_launches": int(args.steps * info["kernels_per_push"]),
             "roofline": roofline,
             "cpu_baseline": cpu,
