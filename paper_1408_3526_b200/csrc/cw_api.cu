@@ -705,16 +705,26 @@ int cw_push(cw_handle *h, const float *frame, float *residual, float *prediction
 #else
         const int nt = 1;
 #endif
-        const long long chunk = ((long long)HW + nt - 1) / nt;
+        // NPIECE pieces: the DMA of piece k overlaps the staging copy of k+1
+        constexpr int NPIECE = 4;
+        const size_t piece = (HW + NPIECE - 1) / NPIECE;
+        for (int k = 0; k < NPIECE; k++) {
+            const size_t p0 = k * piece, p1 = std::min(HW, p0 + piece);
+            if (p0 >= p1)
+                break;
+            const long long chunk = ((long long)(p1 - p0) + nt - 1) / nt;
 #pragma omp parallel for num_threads(nt) schedule(static)
-        for (int t = 0; t < nt; t++) {
-            const long long b = t * chunk, e = std::min((long long)HW, b + chunk);
-            if (b < e)
-                std::memcpy(h->h_stage + b, frame + b, sizeof(float) * (size_t)(e - b));
+            for (int t = 0; t < nt; t++) {
+                const long long b = (long long)p0 + t * chunk, e = std::min((long long)p1, b + chunk);
+                if (b < e)
+                    std::memcpy(h->h_stage + b, frame + b, sizeof(float) * (size_t)(e - b));
+            }
+            CW_CUDA(h, cudaMemcpyAsync(slot + p0, h->h_stage + p0, (p1 - p0) * 4, cudaMemcpyHostToDevice, s));
         }
         src = h->h_stage;
+    } else {
+        CW_CUDA(h, cudaMemcpyAsync(slot, src, HW * 4, cudaMemcpyHostToDevice, s));
     }
-    CW_CUDA(h, cudaMemcpyAsync(slot, src, HW * 4, cudaMemcpyHostToDevice, s));
     if (src == h->h_stage)
         CW_CUDA(h, cudaEventRecord(h->ev_stage, s));
     int32_t rd = 0;
