@@ -139,10 +139,8 @@ def load():
         "cw_launch_info": (ctypes.c_int, [vp, P(i32), P(i32), P(i32), P(i32)]),
         "cw_set_timing": (ctypes.c_int, [vp, i32]),
         "cw_copy_to_host": (ctypes.c_int, [vp, vp, vp, ctypes.c_size_t]),
-        "cw_submit": (ctypes.c_int, [vp, P(ctypes.c_float), P(ctypes.c_float), P(ctypes.c_float),
-                                     P(ctypes.c_uint8), P(i64)]),
-        "cw_submit_raw": (ctypes.c_int, [vp, vp, i32, ctypes.c_double, ctypes.c_double, P(ctypes.c_float),
-                                         P(ctypes.c_float), P(ctypes.c_uint8), P(i64)]),
+        "cw_submit": (ctypes.c_int, [vp, vp, vp, vp, vp, P(i64)]),
+        "cw_submit_raw": (ctypes.c_int, [vp, vp, i32, ctypes.c_double, ctypes.c_double, vp, vp, vp, P(i64)]),
         "cw_wait": (ctypes.c_int, [vp, i64, P(i32), P(i64)]),
         "cw_set_detection": (ctypes.c_int, [vp, ctypes.c_float, i32]),
         "cw_set_backend": (ctypes.c_int, [vp, i32]),

@@ -338,10 +338,9 @@ class Pipeline:
                 raise ValueError(f"frame shape {frame.shape} != {(h, w)}")
             res, pred, vidx = self._pool.take_outputs(h, w)
             ticket = ctypes.c_int64(-1)
-            rc = lib.cw_submit_raw(self._h, ctypes.c_void_p(frame.ctypes.data),
-                                   _native.FMT_PGM16 if pgm else _native.FMT_F32LE, float(scale), float(offset),
-                                   _native.fptr(res), _native.fptr(pred),
-                                   vidx.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), ctypes.byref(ticket))
+            rc = lib.cw_submit_raw(self._h, frame.ctypes.data, _native.FMT_PGM16 if pgm else _native.FMT_F32LE,
+                                   float(scale), float(offset), res.ctypes.data, pred.ctypes.data, vidx.ctypes.data,
+                                   ctypes.byref(ticket))
             _native.check(rc, self._h)
             inflight.append((ticket.value, frame, res, pred, vidx))
             while len(inflight) > depth:
