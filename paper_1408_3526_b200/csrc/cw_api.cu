@@ -680,12 +680,28 @@ static void *mapped_host(const void *p)
     return at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
 }
 
+// cw_push's buffers must be host memory (device frames: cw_push_device)
+static bool is_device_memory(const void *p)
+{
+    if (!p)
+        return false;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice;
+}
+
 int cw_push(cw_handle *h, const float *frame, float *residual, float *prediction, uint8_t *vidx, int32_t *ready,
             int64_t *frame_index, void *stream)
 {
     NvtxRange nvtx("cw_push");
     if (!h || !frame)
         return CW_ERR_VALUE;
+    if (is_device_memory(frame) || is_device_memory(residual) || is_device_memory(prediction) ||
+        is_device_memory(vidx))
+        return fail(h, CW_ERR_VALUE, "cw_push takes host buffers (device frames: cw_push_device)");
     cudaStream_t s = pick_stream(h, stream);
     float *slot;
     cw_next_frame_slot(h, &slot);

@@ -435,3 +435,27 @@ def test_host_buffer_kinds_give_identical_outputs(params):
             assert a[0] == b[0], key
             for x, y in zip(a[1:], b[1:]):
                 assert np.array_equal(x, y), key
+
+
+def test_push_rejects_device_buffers(params):
+    """cw_push is the host-buffer call: device pointers fail with a status
+    code and a message (cw_push_device is the device entry), no crash."""
+    import ctypes
+
+    import torch
+
+    from paper_1408_3526_b200 import Pipeline, _native
+
+    lib = _native.load()
+    with Pipeline(params, 32, 24) as pipe:
+        dev = torch.zeros((24, 32), dtype=torch.float32, device="cuda")
+        r, f = ctypes.c_int32(), ctypes.c_int64()
+        rc = lib.cw_push(pipe._h, dev.data_ptr(), None, None, None, ctypes.byref(r), ctypes.byref(f), None)
+        assert rc == _native.CW_ERR_VALUE
+        assert b"cw_push_device" in lib.cw_last_error(pipe._h)
+        host = np.zeros((24, 32), np.float32)
+        out = np.zeros((24, 32), np.float32)
+        rc = lib.cw_push(pipe._h, host.ctypes.data, dev.data_ptr(), None, None, ctypes.byref(r), ctypes.byref(f), None)
+        assert rc == _native.CW_ERR_VALUE
+        assert pipe.process_frame(host) is None  # the pipeline still works
+        del out
