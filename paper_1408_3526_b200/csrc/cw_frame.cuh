@@ -44,7 +44,10 @@ constexpr int MAXK = 5;    // largest half window supported by the tables
 constexpr int MAXM = 2 * MAXK + 1;
 constexpr int MAXL = 33;   // largest lag grid per axis
 constexpr int LREC = (1 + 2 * MAXK + 3) / 4 * 4;  // floats per lag coefficient record
-constexpr int RESTART = 32;  // rows between direct y-SDFT restarts (bounds f32 drift)
+#ifndef CW_RESTART
+#define CW_RESTART 64
+#endif
+constexpr int RESTART = CW_RESTART;  // rows between direct y-SDFT restarts (bounds f32 drift)
 #ifndef CW_MEMONLY
 #define CW_MEMONLY 0  // diagnostic build: state / T^ / frame / output traffic only (tools: memory floor)
 #endif
