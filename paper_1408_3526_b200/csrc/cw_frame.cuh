@@ -57,6 +57,9 @@ constexpr int RESTART = CW_RESTART;  // rows between direct y-SDFT restarts (bou
 #ifndef CW_ST_NA
 #define CW_ST_NA 1  // state / T^ stores with L1::no_allocate
 #endif
+#ifndef CW_TMA_CHUNKS
+#define CW_TMA_CHUNKS 1  // bulk copies per state packet (1: one copy per row, measured fastest)
+#endif
 #ifndef CW_FENCE_ALL
 #define CW_FENCE_ALL 1  // every thread orders its generic stage reads before the next TMA write
 #endif
@@ -419,7 +422,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
             constexpr uint32_t bs = G::NSP * 32 * 8;
             mbar_expect_tx(bar, bs);
             const unsigned char *src = reinterpret_cast<const unsigned char *>(a.state + pix * G::NSP * 32);
-            constexpr uint32_t CH = (bs / 4 + 15) / 16 * 16;
+            constexpr uint32_t CH = (bs / CW_TMA_CHUNKS + 15) / 16 * 16;
             for (uint32_t off = 0; off < bs; off += CH)
                 tma_load(reinterpret_cast<unsigned char *>(stage) + off, src + off, (bs - off) < CH ? (bs - off) : CH,
                          bar);
