@@ -176,3 +176,25 @@ def test_scene_generator_reproduces_reference_bits():
     frames, comps = generate(SimConfig(width=64, height=64, frame_count=32, rng_seed=0))
     assert np.array_equal(comps, z["components"])
     assert np.array_equal(frames, z["frames"])
+
+
+def test_product_package_never_touches_the_oracle():
+    """The float64 oracle is test infrastructure: no module of the product
+    package imports, loads or names it (static check of the sources)."""
+    import ast
+    import os
+
+    import paper_1408_3526_b200 as pkg
+
+    root = os.path.dirname(pkg.__file__)
+    for name in sorted(os.listdir(root)):
+        if not name.endswith(".py"):
+            continue
+        tree = ast.parse(open(os.path.join(root, name)).read())
+        for node in ast.walk(tree):
+            if isinstance(node, ast.Import):
+                assert not any(a.name.split(".")[0] == "oracle" for a in node.names), name
+            elif isinstance(node, ast.ImportFrom):
+                assert (node.module or "").split(".")[0] != "oracle", name
+            elif isinstance(node, ast.Constant) and isinstance(node.value, str):
+                assert "libcw_oracle" not in node.value, name
