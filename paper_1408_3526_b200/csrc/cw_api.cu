@@ -125,12 +125,37 @@ static int fail(cw_handle *h, int code, const std::string &msg)
     return code;
 }
 
+// Binds the handle's device for the duration of an ABI call and restores the
+// caller's current device on exit: streams, events and lazily allocated
+// buffers belong to h->device, and a launch into a stream of another device
+// fails, so every call that launches, copies, allocates or waits binds it
+// (pipelines on several GPUs may be driven from one thread).
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(const cw_handle *h) : DeviceGuard(h ? h->device : -1) {}
+    explicit DeviceGuard(int device)
+    {
+        if (device >= 0 && cudaGetDevice(&prev) == cudaSuccess && prev != device)
+            cudaSetDevice(device);
+        else
+            prev = -1;
+    }
+    ~DeviceGuard()
+    {
+        if (prev >= 0)
+            cudaSetDevice(prev);
+    }
+};
+
 #define CW_CUDA(h, expr)                                                                  \
     do {                                                                                  \
         cudaError_t _e = (expr);                                                          \
         if (_e != cudaSuccess)                                                            \
             return fail((h), CW_ERR_CUDA, std::string(#expr ": ") + cudaGetErrorString(_e)); \
     } while (0)
+
+// detection buffer: 64-byte header + one f64 sum of squares per (row, block)
+static size_t det_head_bytes(const cw_handle *h) { return 64 + 8 * (size_t)h->H * h->NXB; }
 
 // validate(): the subset of params.py:114-158 that the device path relies on
 // (the Python host layer runs the full rule set with the reference messages).
@@ -435,7 +460,8 @@ int cw_create(const cw_params *p, int32_t width, int32_t height, int32_t device,
         cw_destroy(h);
         return fail(nullptr, code, keep);
     };
-    if (cudaSetDevice(device) != cudaSuccess)
+    DeviceGuard dg(-1);  // restores the caller's current device on return
+    if (cudaGetDevice(&dg.prev) != cudaSuccess || cudaSetDevice(device) != cudaSuccess)
         return cleanup_fail(CW_ERR_CUDA, "cudaSetDevice failed (no CUDA device?)");
     if (cudaStreamCreateWithFlags(&h->own, cudaStreamNonBlocking) != cudaSuccess)
         return cleanup_fail(CW_ERR_CUDA, "cudaStreamCreate failed");
@@ -485,6 +511,7 @@ int cw_create(const cw_params *p, int32_t width, int32_t height, int32_t device,
 
 void cw_destroy(cw_handle *h)
 {
+    DeviceGuard dg(h);
     if (!h)
         return;
     if (h->own)
@@ -599,7 +626,7 @@ static int run_frame(cw_handle *h, cudaStream_t s, int32_t *ready, int64_t *fram
     a.det_cap = h->det_cap;
     if (h->det_on && rd) {
         a.det = h->d_det + set * h->det_bytes;
-        CW_CUDA(h, cudaMemsetAsync(a.det, 0, 64, s));
+        CW_CUDA(h, cudaMemsetAsync(a.det, 0, det_head_bytes(h), s));
     }
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (h->timing) {
@@ -634,7 +661,7 @@ static int run_frame(cw_handle *h, cudaStream_t s, int32_t *ready, int64_t *fram
         CW_CUDA(h, cudaEventRecord(e1, s));
     if (a.det) {  // results to the pinned mirror of this frame (ordered on s)
         CW_CUDA(h, cudaMemcpyAsync(h->h_det + (size_t)(n % cw_handle::NEV) * h->det_bytes, a.det,
-                                   64 + (size_t)h->det_cap * 16, cudaMemcpyDeviceToHost, s));
+                                   h->det_bytes, cudaMemcpyDeviceToHost, s));
     }
     h->frames_seen = n + 1;
     if (rd)
@@ -648,6 +675,7 @@ static int run_frame(cw_handle *h, cudaStream_t s, int32_t *ready, int64_t *fram
 
 int cw_push_inplace(cw_handle *h, int32_t *ready, int64_t *frame_index, void *stream)
 {
+    DeviceGuard dg(h);
     if (!h)
         return CW_ERR_VALUE;
     return run_frame(h, pick_stream(h, stream), ready, frame_index);
@@ -655,6 +683,7 @@ int cw_push_inplace(cw_handle *h, int32_t *ready, int64_t *frame_index, void *st
 
 int cw_push_device(cw_handle *h, const float *frame_dev, int32_t *ready, int64_t *frame_index, void *stream)
 {
+    DeviceGuard dg(h);
     if (!h || !frame_dev)
         return CW_ERR_VALUE;
     cudaStream_t s = pick_stream(h, stream);
@@ -696,6 +725,7 @@ static bool is_device_memory(const void *p)
 int cw_push(cw_handle *h, const float *frame, float *residual, float *prediction, uint8_t *vidx, int32_t *ready,
             int64_t *frame_index, void *stream)
 {
+    DeviceGuard dg(h);
     NvtxRange nvtx("cw_push");
     if (!h || !frame)
         return CW_ERR_VALUE;
@@ -879,6 +909,7 @@ int cw_submit_raw(cw_handle *h, const void *samples, int32_t format, double scal
 static int submit_impl(cw_handle *h, const void *samples, int format, double scale, double offset,
                        float *residual, float *prediction, uint8_t *vidx, int64_t *ticket)
 {
+    DeviceGuard dg(h);
     NvtxRange nvtx("cw_submit");
     const void *frame = samples;
     if (!h || !frame || !ticket)
@@ -933,6 +964,7 @@ static int submit_impl(cw_handle *h, const void *samples, int format, double sca
 
 int cw_wait(cw_handle *h, int64_t ticket, int32_t *ready, int64_t *frame_index)
 {
+    DeviceGuard dg(h);
     if (!h || ticket < 0 || ticket >= h->frames_seen || ticket < h->frames_seen - cw_handle::NEV)
         return h ? fail(h, CW_ERR_VALUE, "unknown or expired ticket") : CW_ERR_VALUE;
     const int e = (int)(ticket % cw_handle::NEV);
@@ -946,13 +978,14 @@ int cw_wait(cw_handle *h, int64_t ticket, int32_t *ready, int64_t *frame_index)
 
 int cw_set_detection(cw_handle *h, float tau, int32_t cap)
 {
+    DeviceGuard dg(h);
     if (!h)
         return CW_ERR_VALUE;
     if (cap < 0) {  // off
         h->det_on = false;
         return CW_OK;
     }
-    const size_t bytes = 64 + (size_t)cap * 16;
+    const size_t bytes = det_head_bytes(h) + (size_t)cap * 16;
     if (bytes != h->det_bytes) {
         CW_CUDA(h, cudaSetDevice(h->device));
         CW_CUDA(h, cudaDeviceSynchronize());
@@ -979,17 +1012,21 @@ int cw_detections(cw_handle *h, int64_t ticket, int32_t *n_total, float *xyr, in
     const unsigned char *b = h->h_det + (size_t)(ticket % cw_handle::NEV) * h->det_bytes;
     unsigned int count;
     unsigned long long key, nval;
-    double sumsq;
     std::memcpy(&count, b, 4);
     std::memcpy(&key, b + 8, 8);
-    std::memcpy(&sumsq, b + 16, 8);
     std::memcpy(&nval, b + 24, 8);
+    double sumsq = 0.0;  // fixed summation order over the (row, block) partial sums
+    for (size_t i = 0; i < (size_t)h->H * h->NXB; i++) {
+        double v;
+        std::memcpy(&v, b + 64 + 8 * i, 8);
+        sumsq += v;
+    }
     if (n_total)
         *n_total = (int32_t)count;
     const int k = (int)std::min<long long>(std::min<long long>(count, h->det_cap), std::max(0, out_cap));
     for (int i = 0; i < k && xyr; i++) {
         float v[4];
-        std::memcpy(v, b + 64 + (size_t)i * 16, 16);
+        std::memcpy(v, b + det_head_bytes(h) + (size_t)i * 16, 16);
         xyr[3 * i] = v[0];
         xyr[3 * i + 1] = v[1];
         xyr[3 * i + 2] = v[2];
@@ -1037,6 +1074,7 @@ int cw_snapshot_size(const cw_handle *h, size_t *bytes)
 
 int cw_snapshot(cw_handle *h, void *dst, size_t bytes)
 {
+    DeviceGuard dg(h);
     size_t need = 0;
     cw_snapshot_size(h, &need);
     if (!h || !dst || bytes != need)
@@ -1058,6 +1096,7 @@ int cw_snapshot(cw_handle *h, void *dst, size_t bytes)
 
 int cw_restore(cw_handle *h, const void *src, size_t bytes)
 {
+    DeviceGuard dg(h);
     size_t need = 0;
     cw_snapshot_size(h, &need);
     if (!h || !src || bytes != need)
@@ -1082,6 +1121,7 @@ int cw_restore(cw_handle *h, const void *src, size_t bytes)
 
 int cw_copy_to_host(cw_handle *h, void *dst, const void *src_dev, size_t bytes)
 {
+    DeviceGuard dg(h);
     if (!h || !dst || !src_dev)
         return CW_ERR_VALUE;
     CW_CUDA(h, cudaMemcpy(dst, src_dev, bytes, cudaMemcpyDeviceToHost));
@@ -1106,6 +1146,7 @@ int cw_launch_info(const cw_handle *h, int32_t *kernels_per_push, int32_t *grid,
 
 int cw_set_backend(cw_handle *h, int32_t naive)
 {
+    DeviceGuard dg(h);
     if (!h)
         return CW_ERR_VALUE;
     if (naive && !h->naive_grid) {
@@ -1133,6 +1174,7 @@ int cw_set_timing(cw_handle *h, int32_t on)
 
 int cw_kernel_time(cw_handle *h, double *total_ms, int64_t *launches)
 {
+    DeviceGuard dg(h);
     if (!h || !total_ms || !launches)
         return CW_ERR_VALUE;
     double tot = 0.0;
@@ -1151,6 +1193,7 @@ int cw_kernel_time(cw_handle *h, double *total_ms, int64_t *launches)
 // Parity views: unpack the packet layout into the reference layouts.
 int cw_read_view(cw_handle *h, int32_t what, void *dst, size_t bytes)
 {
+    DeviceGuard dg(h);
     if (!h || !dst)
         return CW_ERR_VALUE;
     CW_CUDA(h, cudaSetDevice(h->device));

@@ -119,8 +119,9 @@ struct FrameArgs {
     int ready, first;      // flow/PEF enabled; first ready frame (T^ := T)
     int forced_ix, forced_iy;  // < 0: no override
     int mhx, mhy;
-    // detection epilogue (nullable): header {u32 count; u64 peak key;
-    // f64 sum res^2; u64 n valid} then float4 (x, y, res, 0) x det_cap
+    // detection epilogue (nullable): 64-byte header {u32 count; u64 peak
+    // key; -; u64 n valid}, f64 sum res^2 per (local row, column block)
+    // [H * NXB], then float4 (x, y, res, 0) x det_cap
     unsigned char *det;
     float det_tau;  // |res| >= det_tau is a detection (<= 0: list off)
     int det_cap;
@@ -134,9 +135,11 @@ __device__ __forceinline__ void detect_epilogue(const FrameArgs &a, bool valid, 
 {
     unsigned int *count = reinterpret_cast<unsigned int *>(a.det);
     unsigned long long *peak = reinterpret_cast<unsigned long long *>(a.det + 8);
-    double *sumsq = reinterpret_cast<double *>(a.det + 16);
     unsigned long long *nval = reinterpret_cast<unsigned long long *>(a.det + 24);
-    float4 *list = reinterpret_cast<float4 *>(a.det + 64);
+    // sum res^2 per (row, 32-column block) slot, summed on the host in a
+    // fixed order: the metric is bit-reproducible run to run
+    double *sumsq = reinterpret_cast<double *>(a.det + 64);
+    float4 *list = reinterpret_cast<float4 *>(a.det + 64 + 8 * (size_t)a.H * a.NXB);
     const float v = fabsf(res);
     if (valid && a.det_tau > 0.f && v >= a.det_tau) {
         const unsigned int slot = atomicAdd(count, 1u);
@@ -155,7 +158,7 @@ __device__ __forceinline__ void detect_epilogue(const FrameArgs &a, bool valid, 
     const unsigned int nv = __popc(__ballot_sync(0xffffffffu, valid));
     if ((threadIdx.x & 31) == 0 && nv) {
         atomicMax(peak, key);
-        atomicAdd(sumsq, sq);
+        sumsq[(size_t)(oy + a.mhy) * a.NXB + (ox + a.mhx) / 32] = sq;
         atomicAdd(nval, (unsigned long long)nv);
     }
 }

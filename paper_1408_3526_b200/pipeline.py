@@ -13,8 +13,17 @@ Differences from the reference, by design:
 * ``spectrum_backend="naive"`` (the reference's non-recursive backend,
   spectrum.py:257-327) evaluates every pixel's window DFT directly on the
   GPU (csrc/cw_naive.cuh) and feeds the same fused flow/PEF kernel.
-* ``imag_peak`` is 0.0 by construction: the PEF sums conjugate bin pairs,
-  so the prediction is real without a discarded imaginary residue.
+* ``imag_peak`` (max |Im acc|, pipeline.py:293) is evaluated from the
+  folded imaginary PEF coefficients: the kernel stores the half spectrum
+  (S(-k) = conj S(k) exactly), so Im acc = sum S.re (c.im + c'.im) +
+  S.im (c.re - c'.re) over the pairs (k, -k).  For a Hermitian bank (every
+  bank ``build_bank`` makes: c(-k) = conj c(k) bit for bit) all those
+  coefficients are exactly 0 and so is imag_peak; an injected non-Hermitian
+  bank gets it computed from the device spectrum (``process_frame`` only).
+* ``last_timings`` has the reference's keys (pipeline.py:210-285); the
+  stages run fused in one kernel, so "conditioning", "autocorr" and
+  "filtering" are 0.0 and "spectrum" holds the whole call; with
+  ``device_timing=True`` "kernel" adds the fused kernel's device time.
 """
 
 from __future__ import annotations
@@ -105,23 +114,17 @@ class _PinnedPool:
     the array handed out (and every view of it) has been garbage collected.
     """
 
+    # pinned bytes handed out at once before further outputs fall back to
+    # ordinary (pageable) numpy arrays: callers that keep every residual
+    # (cli._cmd_filter appends them all) must not pin unbounded host memory
+    MAX_OUTSTANDING_BYTES = 256 << 20
+
     def __init__(self):
         self._free: dict[tuple, list] = {}
-        self._lock = threading.Lock()
-
-    def take(self, shape, dtype):
-        import torch
-
-        key = (tuple(shape), np.dtype(dtype).str)
-        with self._lock:
-            stack = self._free.setdefault(key, [])
-            tensor = stack.pop() if stack else None
-        if tensor is None:
-            tdt = {np.dtype(np.float32): torch.float32, np.dtype(np.uint8): torch.uint8}[np.dtype(dtype)]
-            tensor = torch.empty(shape, dtype=tdt, pin_memory=True)
-        arr = tensor.numpy()
-        weakref.finalize(arr, self._give, key, tensor)
-        return arr
+        # re-entrant: _give runs from weakref finalizers, which cyclic GC may
+        # fire on this thread while take/take_outputs holds the lock
+        self._lock = threading.RLock()
+        self._outstanding = 0
 
     def take_outputs(self, h, w):
         """(residual, prediction, velocity-index) arrays of one call, carved
@@ -132,20 +135,28 @@ class _PinnedPool:
         key = ("outputs", h, w)
         hw = h * w
         with self._lock:
-            stack = self._free.setdefault(key, [])
-            tensor = stack.pop() if stack else None
-        if tensor is None:
-            tensor = torch.empty(10 * hw, dtype=torch.uint8, pin_memory=True)
-        blk = tensor.numpy()
-        weakref.finalize(blk, self._give, key, tensor)
+            if self._outstanding + 10 * hw > self.MAX_OUTSTANDING_BYTES and self._outstanding > 0:
+                tensor = False  # pool exhausted: pageable arrays (the device copies through staging)
+            else:
+                stack = self._free.setdefault(key, [])
+                tensor = stack.pop() if stack else None
+                self._outstanding += 10 * hw
+        if tensor is False:
+            blk = np.empty(10 * hw, np.uint8)
+        else:
+            if tensor is None:
+                tensor = torch.empty(10 * hw, dtype=torch.uint8, pin_memory=True)
+            blk = tensor.numpy()
+            weakref.finalize(blk, self._give, key, tensor, 10 * hw)
         res = blk[: 4 * hw].view(np.float32).reshape(h, w)
         pred = blk[4 * hw : 8 * hw].view(np.float32).reshape(h, w)
         vidx = blk[8 * hw :].reshape(h, w, 2)
         return res, pred, vidx
 
-    def _give(self, key, tensor):
+    def _give(self, key, tensor, nbytes):
         with self._lock:
             self._free.setdefault(key, []).append(tensor)
+            self._outstanding -= nbytes
 
 
 @dataclass
@@ -223,6 +234,10 @@ class Pipeline:
         self._lut_v = np.stack([self._lag_x[ix], self._lag_y[iy]], axis=-1)
         self._pool = _PinnedPool()
 
+        # folded imaginary PEF coefficients c(k).im + c(-k).im, c(k).re - c(-k).re
+        cf = np.asarray(bank.coeffs)
+        self._hermitian = bool(np.all(cf == np.conj(cf[:, :, ::-1, ::-1, ::-1])))
+
         self._forced = None
         if forced_velocity is not None:
             ix, iy = bank.index_of(forced_velocity)
@@ -288,14 +303,44 @@ class Pipeline:
         rc = lib.cw_push(self._h, frame.ctypes.data, res.ctypes.data, pred.ctypes.data, vidx.ctypes.data,
                          ctypes.byref(ready), ctypes.byref(fidx), None)
         _native.check(rc, self._h)
-        self.last_timings = {"pipeline": time.perf_counter() - t0}
-        if self._device_timing:
-            ms, n = ctypes.c_double(), ctypes.c_int64()
-            _native.check(lib.cw_kernel_time(self._h, ctypes.byref(ms), ctypes.byref(n)), self._h)
-            self.last_timings["kernel"] = ms.value / 1e3
+        self._set_timings(time.perf_counter() - t0, bool(ready.value))
         if not ready.value:
             return None
-        return self._wrap(int(fidx.value), res, pred, vidx, ticket=self.frames_seen - 1)
+        out = self._wrap(int(fidx.value), res, pred, vidx, ticket=self.frames_seen - 1)
+        if not self._hermitian:
+            out.imag_peak = self._imag_peak_from_state(vidx)
+        return out
+
+    def _set_timings(self, seconds: float, ready: bool) -> None:
+        """Reference keys (pipeline.py:210-285): warm-up frames report
+        spectrum + pipeline, ready frames all five stages; the fused stages
+        after the spectrum take no time of their own."""
+        t = {"spectrum": seconds}
+        if ready:
+            t.update(conditioning=0.0, autocorr=0.0, filtering=0.0)
+        t["pipeline"] = seconds
+        if self._device_timing:
+            ms, n = ctypes.c_double(), ctypes.c_int64()
+            lib = _native.load()
+            _native.check(lib.cw_kernel_time(self._h, ctypes.byref(ms), ctypes.byref(n)), self._h)
+            t["kernel"] = ms.value / 1e3
+        self.last_timings = t
+
+    def _imag_peak_from_state(self, vidx) -> float:
+        """max |Im sum_j c_j S_j| over the valid outputs (_kernels.py:338-341)
+        for a non-Hermitian bank, from the spectrum of the frame just run."""
+        p = self.params
+        spec = self.spectrum()
+        x0, x1, y0, y1 = valid_bounds(p, self.width, self.height)
+        mhx, mhy, _ = p.mhat
+        cy, cx = p.ky, p.kx
+        band = spec[y0 + mhy:y1 + mhy + 1, x0 + mhx:x1 + mhx + 1, :,
+                    cy - p.by:cy + p.by + 1, cx - p.bx:cx + p.bx + 1]
+        v = vidx[y0 + mhy:y1 + mhy + 1, x0 + mhx:x1 + mhx + 1]
+        coef = np.asarray(self.bank.coeffs, np.complex128)[v[..., 1], v[..., 0]]
+        imag = np.abs(np.einsum("...k,...k->...", coef.reshape(coef.shape[:2] + (-1,)),
+                                band.reshape(band.shape[:2] + (-1,))).imag)
+        return float(imag.astype(np.float32).max()) if imag.size else 0.0
 
     def process_stream(self, frames, depth: int = 3, sample_format: str = "f32le",
                        scale: float = 1.0, offset: float = 0.0):
@@ -332,25 +377,35 @@ class Pipeline:
             _native.check(lib.cw_wait(self._h, ticket, ctypes.byref(ready), ctypes.byref(fidx)), self._h)
             return self._wrap(int(fidx.value), res, pred, vidx, ticket=ticket) if ready.value else None
 
-        for frame in frames:
-            frame = np.ascontiguousarray(frame, dtype=">u2" if pgm else np.float32)
-            if frame.shape != (h, w):
-                raise ValueError(f"frame shape {frame.shape} != {(h, w)}")
-            res, pred, vidx = self._pool.take_outputs(h, w)
-            ticket = ctypes.c_int64(-1)
-            rc = lib.cw_submit_raw(self._h, frame.ctypes.data, _native.FMT_PGM16 if pgm else _native.FMT_F32LE,
-                                   float(scale), float(offset), res.ctypes.data, pred.ctypes.data, vidx.ctypes.data,
-                                   ctypes.byref(ticket))
-            _native.check(rc, self._h)
-            inflight.append((ticket.value, frame, res, pred, vidx))
-            while len(inflight) > depth:
+        try:
+            for frame in frames:
+                frame = np.ascontiguousarray(frame, dtype=">u2" if pgm else np.float32)
+                if frame.shape != (h, w):
+                    raise ValueError(f"frame shape {frame.shape} != {(h, w)}")
+                res, pred, vidx = self._pool.take_outputs(h, w)
+                ticket = ctypes.c_int64(-1)
+                rc = lib.cw_submit_raw(self._h, frame.ctypes.data, _native.FMT_PGM16 if pgm else _native.FMT_F32LE,
+                                       float(scale), float(offset), res.ctypes.data, pred.ctypes.data,
+                                       vidx.ctypes.data, ctypes.byref(ticket))
+                _native.check(rc, self._h)
+                inflight.append((ticket.value, frame, res, pred, vidx))
+                while len(inflight) > depth:
+                    out = collect(inflight.popleft())
+                    if out is not None:
+                        yield out
+            while inflight:
                 out = collect(inflight.popleft())
                 if out is not None:
                     yield out
-        while inflight:
-            out = collect(inflight.popleft())
-            if out is not None:
-                yield out
+        finally:
+            # the caller stopped early (break / close / GC) or a call failed:
+            # wait for every outstanding frame before its pinned output block
+            # (and input frame) can be recycled, so that no queued D2H copy
+            # lands in a block a later call already owns
+            while inflight:
+                ticket = inflight.popleft()[0]
+                if self._h:
+                    lib.cw_wait(self._h, ticket, None, None)
 
     def process_frame_device(self, frame) -> WhitenedOutput | None:
         """``process_frame`` for a frame already in device memory: a CUDA
@@ -378,7 +433,7 @@ class Pipeline:
         _native.check(rc, self._h)
         stream.synchronize()
         if not ready.value:
-            self.last_timings = {"pipeline": time.perf_counter() - t0}
+            self._set_timings(time.perf_counter() - t0, False)
             return None
         res_p, pred_p, vidx_p = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
         _native.check(lib.cw_device_outputs(self._h, ctypes.byref(res_p), ctypes.byref(pred_p),
@@ -389,14 +444,17 @@ class Pipeline:
         vidx = np.empty((h, w, 2), np.uint8)
         for dst, src in ((res, res_p), (pred, pred_p), (vidx, vidx_p)):
             _native.check(lib.cw_copy_to_host(self._h, dst.ctypes.data, src, dst.nbytes), self._h)
-        self.last_timings = {"pipeline": time.perf_counter() - t0}
-        return self._wrap(int(fidx.value), res, pred, vidx, ticket=self.frames_seen - 1)
+        self._set_timings(time.perf_counter() - t0, True)
+        out = self._wrap(int(fidx.value), res, pred, vidx, ticket=self.frames_seen - 1)
+        if not self._hermitian:
+            out.imag_peak = self._imag_peak_from_state(vidx)
+        return out
 
     def _wrap(self, frame_index, res, pred, vidx, ticket=None) -> WhitenedOutput:
         codes = vidx.view(np.uint16).reshape(vidx.shape[:2])
         out = WhitenedOutput(frame_index=frame_index, residual=res, prediction=pred,
                              velocity=_LazyVelocityField(codes, self._lut_i, self._lut_v),
-                             mask=self.mask, imag_peak=0.0)
+                             mask=self.mask, imag_peak=0.0 if self._hermitian else float("nan"))
         if self._detect and ticket is not None:
             out.detections, out.metrics = self._fetch_detections(ticket)
         return out

@@ -203,16 +203,23 @@ def _stream(reader: SequenceReader, pipe: Pipeline, consume, *, want_pred: bool,
         ready_in.put(None)
 
     def write_loop():
-        try:
-            while True:
-                item = to_write.get()
-                if item is None:
-                    return
-                fidx, t_in, outs, stats = item
-                consume(fidx, t_in, outs[0], outs[1], outs[2], stats)
-                free_out.put(outs)
-        except BaseException as exc:
-            errors.append(exc)
+        # After a failed consume() the loop keeps draining to_write (without
+        # consuming) so that every output set goes back to free_out and the
+        # calling thread, blocked in free_out.get() or to_write.put(), wakes
+        # up, sees `errors` and stops submitting.
+        failed = False
+        while True:
+            item = to_write.get()
+            if item is None:
+                return
+            fidx, t_in, outs, stats = item
+            if not failed:
+                try:
+                    consume(fidx, t_in, outs[0], outs[1], outs[2], stats)
+                except BaseException as exc:
+                    errors.append(exc)
+                    failed = True
+            free_out.put(outs)
 
     inflight = []
 
@@ -255,9 +262,13 @@ def _stream(reader: SequenceReader, pipe: Pipeline, consume, *, want_pred: bool,
             inflight.append((ticket.value, buf, (res, pred, vidx)))
             while len(inflight) > depth:
                 collect()
-        while inflight:
+        while inflight and not errors:
             collect()
     finally:
+        # never leave a DMA in flight into buffers this function drops
+        for ticket, _buf, _outs in inflight:
+            lib.cw_wait(pipe._h, ticket, None, None)
+        inflight.clear()
         free_in.put(None)  # unblock the reader if it waits for a buffer
         to_write.put(None)
         writer_t.join()
@@ -295,13 +306,13 @@ def filter_sequence(input_dir, out_dir, params: FilterParams | None = None, *, d
                 res_w.append(res)
                 if pred_w is not None:
                     pred_w.append(pred)
-                vel = None
-                if vel_fh is not None or (want_metrics and truth is not None):
-                    vel = np.take(lut_v, vidx.view(np.uint16).reshape(h, w), axis=0)
+                codes = vidx.view(np.uint16).reshape(h, w)
                 if vel_fh is not None:
-                    vel_fh.write(vel.data)
+                    vel_fh.write(np.take(lut_v, codes, axis=0).data)
                 if want_metrics:
-                    velocity = None if vel is None else SimpleNamespace(velocities=vel.astype(np.float64))
+                    # metrics from the float64 lags, as cli.compute_metrics_row
+                    velocity = (None if truth is None
+                                else SimpleNamespace(velocities=np.take(pipe._lut_v, codes, axis=0)))
                     rows.append(metrics_row(_Out(fidx, res, pipe.mask, velocity, stats), params, truth))
 
             try:

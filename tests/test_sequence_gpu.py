@@ -178,7 +178,7 @@ def test_filter_sequence_ground_truth_metrics(params, tmp_path):
         o.frame_index, o.residual, o.mask, o.metrics = fidx[k], res[k], mask, None
 
         class V:
-            velocities = np.stack([lag[idx[k][..., 0]], lag[idx[k][..., 1]]], -1).astype(np.float32).astype(np.float64)
+            velocities = np.stack([lag[idx[k][..., 0]], lag[idx[k][..., 1]]], -1)  # float64 lags, as cli.py
         o.velocity = V
         assert line == metrics_row(o, params, gt).csv()
         assert line.split(",")[7] in ("0", "1")
