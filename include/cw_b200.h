@@ -194,6 +194,34 @@ int cw_launch_info(const cw_handle *h, int32_t *kernels_per_push, int32_t *grid,
 int cw_set_timing(cw_handle *h, int32_t on);
 int cw_kernel_time(cw_handle *h, double *total_ms, int64_t *launches);
 
+/*
+ * Counter-based synthetic scene (the model of the
+ * reference generator, scenegen.py:152-209, with noise that is a pure
+ * function of (seed, t, y, x) instead of one row-major numpy stream,
+ * scenegen.py:132-139).  cw_scene_generate writes frames t0 .. t0+n-1,
+ * rows [r0, r1), columns [c0, c1) of the (width x height) scene into
+ * out_dev (n, r1-r0, c1-c0) float32 on the current device, on `stream`.
+ * Any window equals the same pixels of the full frame bit for bit, and
+ * scenegen.generate_counter computes the same bits on the host.
+ */
+typedef struct cw_scene {
+    int32_t width, height;
+    int64_t frame_count;        /* the target reaches the centre at frame_count - 1 */
+    int32_t n_comp;             /* <= 64 drifting cosines */
+    const double *comps;        /* host (n_comp, 4): fx, fy, phase, amplitude */
+    double dc_offset, clutter_vx, clutter_vy;
+    int32_t nonuniform;         /* config C2: v += (ax sin(2 pi y/H), ay cos(2 pi x/W)) */
+    double motion_ax, motion_ay;
+    int32_t target;             /* 0: no point target */
+    double target_vx, target_vy, target_peak, psf_sigma, target_truncation;
+    double noise_sigma;
+    uint64_t seed;
+} cw_scene;
+
+int cw_scene_generate(const cw_scene *scene, int64_t t0, int32_t n_frames, int32_t r0, int32_t r1, int32_t c0,
+                      int32_t c1, float *out_dev, void *stream);
+const char *cw_scene_last_error(void);
+
 /* Library/ABI identification. */
 int32_t cw_abi_version(void);
 

@@ -35,6 +35,7 @@ EXPORTS = (
     "cw_frames_seen", "cw_read_view", "cw_launch_info", "cw_set_timing",
     "cw_kernel_time", "cw_copy_to_host", "cw_submit", "cw_submit_raw", "cw_wait", "cw_set_detection", "cw_detections",
     "cw_set_backend", "cw_snapshot_size", "cw_snapshot", "cw_restore",
+    "cw_scene_generate", "cw_scene_last_error",
 )
 
 
@@ -80,6 +81,10 @@ def build(verbose: bool = False, out: str | None = None, dev: bool = False, extr
             defs = [f"-DCW_{k}={v}" for k, v in zip(("IKX", "IKY", "IKZ", "IBX", "IBY", "INL"), inst)]
             obj = os.path.join(tmp, "cw_inst_" + "_".join(map(str, inst)) + ".o")
             jobs.append(["nvcc", *base, *defs, "-c", "-o", obj, os.path.join(CSRC, "cw_inst.cu")])
+        # the scene generator must not contract a*b+c into FMAs: its numpy
+        # twin (scenegen.generate_counter) rounds every operation
+        jobs.append(["nvcc", *base, "-fmad=false", "-c", "-o", os.path.join(tmp, "cw_scene.o"),
+                     os.path.join(CSRC, "cw_scene.cu")])
         with cf.ThreadPoolExecutor(max_workers=max(1, os.cpu_count() or 1)) as ex:
             results = list(ex.map(lambda c: subprocess.run(c, capture_output=True, text=True), jobs))
         for c, r in zip(jobs, results):
@@ -92,6 +97,18 @@ def build(verbose: bool = False, out: str | None = None, dev: bool = False, extr
                         *(["-lgomp"] if openmp else [])],
                        check=True)
     return out
+
+
+class cw_scene(ctypes.Structure):
+    _fields_ = [
+        ("width", ctypes.c_int32), ("height", ctypes.c_int32), ("frame_count", ctypes.c_int64),
+        ("n_comp", ctypes.c_int32), ("comps", ctypes.POINTER(ctypes.c_double)),
+        ("dc_offset", ctypes.c_double), ("clutter_vx", ctypes.c_double), ("clutter_vy", ctypes.c_double),
+        ("nonuniform", ctypes.c_int32), ("motion_ax", ctypes.c_double), ("motion_ay", ctypes.c_double),
+        ("target", ctypes.c_int32), ("target_vx", ctypes.c_double), ("target_vy", ctypes.c_double),
+        ("target_peak", ctypes.c_double), ("psf_sigma", ctypes.c_double), ("target_truncation", ctypes.c_double),
+        ("noise_sigma", ctypes.c_double), ("seed", ctypes.c_uint64),
+    ]
 
 
 class cw_params(ctypes.Structure):
@@ -149,6 +166,8 @@ def load():
         "cw_restore": (ctypes.c_int, [vp, vp, ctypes.c_size_t]),
         "cw_detections": (ctypes.c_int, [vp, i64, P(i32), P(ctypes.c_float), i32, P(ctypes.c_double)]),
         "cw_kernel_time": (ctypes.c_int, [vp, P(ctypes.c_double), P(i64)]),
+        "cw_scene_generate": (ctypes.c_int, [P(cw_scene), i64, i32, i32, i32, i32, i32, vp, vp]),
+        "cw_scene_last_error": (ctypes.c_char_p, []),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

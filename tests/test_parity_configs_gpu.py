@@ -1,0 +1,305 @@
+"""Parity on every BASELINE.json configuration, the fused
+sm_100a path against the live float64 oracle (oracle/, pinned bit-exactly
+to the reference by tests/test_oracle_golden.py), on the counter-based
+scenes of csrc/cw_scene.cu:
+
+* C2  256x256 x 256 frames, non-uniform motion: every frame, full frame
+* C3  640x512: frames 0-63 full frame, and a 128x128 crop over all 1000
+      frames with spectrum and R^ per-pixel checks along the way
+* C4  4096x4096 x 200 frames through 8 strip pipelines (halo + row offset,
+      strips.py): 8 crops of 256x256 straddling the strip boundaries
+* C5  1280x1024, one 256x256 crop per sweep parameter set
+
+Crops run the oracle on the crop plus its causal margin (My-1 rows above,
+Mx-1 columns left: the window is backward-indexed, _kernels.py:31-68), so
+every crop anchor sees exactly the full-frame input.  Tolerances are
+tests/parity.py's: velocity agreement >= 99.9% of anchors per frame,
+residual <= 1e-4 max|I| where the velocity agrees, spectrum and R^ per
+pixel <= 1e-5.  The residual error over ALL valid outputs (including the
+anchors whose velocity flipped on a near-tie) is reported next to it and
+bounded by ALL_RES_TOL.  Set CW_PARITY_REPORT=<path> to collect the
+measured figures as JSON lines.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from parity import RES_TOL, RHAT_TOL, SPEC_TOL, VEL_FRAC, per_pixel_rel
+
+pytestmark = pytest.mark.gpu
+
+ALL_RES_TOL = 1e-2  # all valid outputs, flipped near-ties included (measured ~2e-3)
+
+
+def _report(**kw):
+    path = os.environ.get("CW_PARITY_REPORT")
+    if path:
+        with open(path, "a") as fh:
+            fh.write(json.dumps(kw) + "\n")
+
+
+class _Stats:
+    """Running parity figures of one configuration."""
+
+    def __init__(self, name):
+        self.name = name
+        self.frames = 0
+        self.vel_min = 1.0
+        self.flips = 0
+        self.anchors = 0
+        self.res_agree = 0.0
+        self.res_all = 0.0
+
+    def add(self, gi, ri, gres, rres, out_valid, fmax):
+        """gi / ri: (h, w, 2) anchor indices; gres / rres: residuals of the
+        same anchors' outputs (anchor - mhat), out_valid: their validity."""
+        same = np.all(gi == ri, axis=-1)
+        frac = float(same.mean())
+        self.frames += 1
+        self.vel_min = min(self.vel_min, frac)
+        self.flips += int((~same).sum())
+        self.anchors += same.size
+        err = np.abs(gres.astype(np.float64) - rres) / fmax
+        if (same & out_valid).any():
+            self.res_agree = max(self.res_agree, float(err[same & out_valid].max()))
+        if out_valid.any():
+            self.res_all = max(self.res_all, float(err[out_valid].max()))
+        assert frac >= VEL_FRAC, f"{self.name}: velocity agreement {frac:.5f}"
+        assert self.res_agree <= RES_TOL, f"{self.name}: residual {self.res_agree:.2e}"
+        assert self.res_all <= ALL_RES_TOL, f"{self.name}: all-pixel residual {self.res_all:.2e}"
+
+    def done(self, **extra):
+        _report(config=self.name, frames=self.frames, vel_agreement_min=self.vel_min,
+                flipped_anchors=self.flips, anchors=self.anchors, res_err_agreeing=self.res_agree,
+                res_err_all_valid=self.res_all, **extra)
+        assert self.frames > 0
+
+
+def _crop_check(st, params, gpu_idx, gpu_res, ref, y0, x0, n_y, n_x, oy, ox, fmax):
+    """Compare anchors [y0, y0+n_y) x [x0, x0+n_x) of a full-frame (or strip)
+    output with the oracle output of the crop whose origin is (oy, ox)."""
+    mhx, mhy, _ = params.mhat
+    gi = gpu_idx[y0:y0 + n_y, x0:x0 + n_x]
+    ri = ref["indices"][y0 - oy:y0 - oy + n_y, x0 - ox:x0 - ox + n_x]
+    gres = gpu_res[y0 - mhy:y0 - mhy + n_y, x0 - mhx:x0 - mhx + n_x]
+    rres = ref["residual"][y0 - oy - mhy:y0 - oy - mhy + n_y, x0 - ox - mhx:x0 - ox - mhx + n_x]
+    st.add(gi, ri, gres, rres, np.ones(gi.shape[:2], bool), fmax)
+
+
+def _oracle(params, w, h):
+    from oracle.oracle import OraclePipeline
+
+    return OraclePipeline(params, w, h)
+
+
+def test_c2_full_run_nonuniform_motion(params):
+    """C2: 256x256 x 256 frames, non-uniform background motion (seed 2),
+    every output frame over the whole frame."""
+    from paper_1408_3526_b200 import Pipeline
+    from paper_1408_3526_b200.scenegen import SimConfig, generate_device
+
+    cfg = SimConfig(width=256, height=256, frame_count=256, rng_seed=2)
+    frames = generate_device(cfg, nonuniform=True).cpu().numpy()
+    fmax = float(np.abs(frames).max())
+    st = _Stats("C2 256x256x256 nonuniform, full frame")
+    with Pipeline(params, 256, 256) as gpu, _oracle(params, 256, 256) as orc:
+        for f in frames:
+            g, r = gpu.process_frame(f), orc.process_frame(f)
+            assert (g is None) == (r is None)
+            if g is None:
+                continue
+            assert g.frame_index == r["frame_index"]
+            m = g.mask
+            mhx, mhy, _ = params.mhat
+            # anchors (y, x) >= (My-1, Mx-1) <-> outputs at anchor - mhat
+            ay, ax = params.my - 1, params.mx - 1
+            _crop_check(st, params, g.velocity.indices, g.residual, r, ay, ax, 256 - ay, 256 - ax, 0, 0, fmax)
+            assert np.all(g.residual[~m] == 0)
+    st.done()
+    assert st.frames == 252
+
+
+def test_c3_full_frames_0_to_63(params):
+    """C3 geometry 640x512, frames 0-63, whole frame; spectrum and R^ per
+    pixel at frame 63."""
+    from paper_1408_3526_b200 import Pipeline
+    from paper_1408_3526_b200.pipeline import rhat_from_state
+    from paper_1408_3526_b200.scenegen import SimConfig, generate_device
+
+    cfg = SimConfig(width=640, height=512, frame_count=1000, rng_seed=0)
+    frames = generate_device(cfg, frames=64).cpu().numpy()
+    fmax = float(np.abs(frames).max())
+    st = _Stats("C3 640x512 frames 0-63, full frame")
+    ay, ax = params.my - 1, params.mx - 1
+    with Pipeline(params, 640, 512) as gpu, _oracle(params, 640, 512) as orc:
+        for f in frames:
+            g, r = gpu.process_frame(f), orc.process_frame(f)
+            if g is None:
+                assert r is None
+                continue
+            assert g.frame_index == r["frame_index"]
+            _crop_check(st, params, g.velocity.indices, g.residual, r, ay, ax, 512 - ay, 640 - ax, 0, 0, fmax)
+        spec = gpu.spectrum()[ay:, ax:]
+        sref = orc.sbins()[ay:, ax:]
+        spec_err = per_pixel_rel(spec, sref, axes=(2, 3, 4))
+        del spec, sref
+        rh = rhat_from_state(gpu.smoothed_state()[ay:, ax:], params)
+        rh_err = per_pixel_rel(rh, orc.rhat()[ay:, ax:], axes=(2, 3))
+    assert spec_err <= SPEC_TOL and rh_err <= RHAT_TOL
+    st.done(spectrum_err_frame63=spec_err, rhat_err_frame63=rh_err)
+
+
+def test_c3_crop_over_all_1000_frames(params):
+    """C3: a 128x128 crop (+ causal margin) over all 1000 frames of the
+    640x512 sequence -- the smoothing pole's steady state (alpha = e^-0.1,
+    10-frame e-folding) and f32 drift over a long run; spectrum and R^ per
+    pixel at frames 100, 500 and 999."""
+    import torch
+
+    from paper_1408_3526_b200 import Pipeline
+    from paper_1408_3526_b200.pipeline import rhat_from_state
+    from paper_1408_3526_b200.scenegen import SimConfig, generate_device
+
+    cfg = SimConfig(width=640, height=512, frame_count=1000, rng_seed=0)
+    y0, x0, n = 200, 300, 128
+    oy, ox = y0 - (params.my - 1), x0 - (params.mx - 1)
+    st = _Stats("C3 640x512 crop 128x128 @ (200,300), frames 0-999")
+    spec_errs, rh_errs = {}, {}
+    fmax = 0.0
+    with Pipeline(params, 640, 512) as gpu, _oracle(params, n + x0 - ox, n + y0 - oy) as orc:
+        for t0 in range(0, 1000, 100):
+            chunk = generate_device(cfg, frames=100, t0=t0)
+            crop = chunk[:, oy:y0 + n, ox:x0 + n].cpu().numpy()
+            fmax = max(fmax, float(chunk.abs().max()))
+            for k in range(100):
+                t = t0 + k
+                g = gpu.process_frame_device(chunk[k])
+                r = orc.process_frame(crop[k])
+                if g is None:
+                    continue
+                _crop_check(st, params, g.velocity.indices, g.residual, r, y0, x0, n, n, oy, ox, fmax)
+                if t in (100, 500, 999):
+                    spec = gpu.spectrum()[y0:y0 + n, x0:x0 + n]
+                    spec_errs[t] = per_pixel_rel(spec, orc.sbins()[y0 - oy:, x0 - ox:], axes=(2, 3, 4))
+                    rh = rhat_from_state(gpu.smoothed_state()[y0:y0 + n, x0:x0 + n], params)
+                    rh_errs[t] = per_pixel_rel(rh, orc.rhat()[y0 - oy:, x0 - ox:], axes=(2, 3))
+                    del spec
+            del chunk
+            torch.cuda.empty_cache()
+    assert st.frames == 996
+    assert max(spec_errs.values()) <= SPEC_TOL and max(rh_errs.values()) <= RHAT_TOL
+    st.done(spectrum_err=spec_errs, rhat_err=rh_errs)
+
+
+C5_SETS = [
+    # (kx, ky, kz, bx, by, lag step): SURVEY §8d, mhat = (kx, ky, kz)
+    (4, 4, 2, 3, 3, 0.25), (3, 3, 2, 2, 2, 0.25), (5, 5, 2, 4, 4, 0.25),
+    (4, 4, 1, 3, 3, 0.25), (4, 4, 2, 3, 3, 0.5), (4, 4, 2, 3, 3, 0.125),
+]
+
+
+@pytest.mark.parametrize("k", range(len(C5_SETS)))
+def test_c5_sweep_crop(k):
+    """C5: 1280x1024 stream k (seed k) with sweep parameter set k; a 256x256
+    crop (+ causal margin) over 64 frames."""
+    import torch
+
+    from paper_1408_3526_b200 import FilterParams, Pipeline
+    from paper_1408_3526_b200.scenegen import SimConfig, generate_device
+
+    kx, ky, kz, bx, by, step = C5_SETS[k]
+    lim = min(2 * kx, 2 * ky) // 2
+    lags = tuple(i * step for i in range(-int(round(2 / step)), int(round(2 / step)) + 1) if abs(i * step) <= lim)
+    p = FilterParams(kx=kx, ky=ky, kz=kz, bx=bx, by=by, mhat=(kx, ky, kz), lag_grid_x=lags, lag_grid_y=lags)
+    cfg = SimConfig(width=1280, height=1024, frame_count=200, rng_seed=k)
+    frames = generate_device(cfg, frames=64)
+    y0, x0, n = 500, 600, 256
+    oy, ox = y0 - (p.my - 1), x0 - (p.mx - 1)
+    crop = frames[:, oy:y0 + n, ox:x0 + n].cpu().numpy()
+    fmax = float(frames.abs().max())
+    st = _Stats(f"C5 1280x1024 {C5_SETS[k]} crop 256x256, 64 frames")
+    with Pipeline(p, 1280, 1024) as gpu, _oracle(p, n + x0 - ox, n + y0 - oy) as orc:
+        for t in range(64):
+            g = gpu.process_frame_device(frames[t])
+            r = orc.process_frame(crop[t])
+            assert (g is None) == (r is None)
+            if g is not None:
+                _crop_check(st, p, g.velocity.indices, g.residual, r, y0, x0, n, n, oy, ox, fmax)
+    del frames
+    torch.cuda.empty_cache()
+    st.done(params=list(C5_SETS[k]), lags=len(lags))
+
+
+def test_c4_strip_boundary_crops(params):
+    """C4: 4096x4096 x 200 frames, split into 8 strips (each with its 8
+    halo rows and row offset, strips.plan_strips); 8 crops of 256x256
+    straddling the strip boundaries (and the top edge) against the oracle."""
+    import torch
+
+    from paper_1408_3526_b200 import Pipeline
+    from paper_1408_3526_b200.scenegen import SimConfig, generate_device
+    from paper_1408_3526_b200.strips import plan_strips
+
+    W = H = 4096
+    T = 200
+    cfg = SimConfig(width=W, height=H, frame_count=T, rng_seed=4)
+    plans = plan_strips(params, H, 8)
+    # crop anchor origins: 7 strip boundaries at different columns + the top edge
+    crops = [(pl.a0 - 128, 300 + 480 * g) for g, pl in enumerate(plans) if g > 0] + [(8, 3800)]
+    n = 256
+    mhx, mhy, _ = params.mhat
+    my, mx = params.my, params.mx
+    pipes = [Pipeline(params, W, pl.local_height, _strip=(pl.halo, pl.lo)) for pl in plans]
+    gpu_idx = {c: [] for c in crops}
+    gpu_res = {c: [] for c in crops}
+    fmax = 0.0
+    try:
+        for t in range(T):
+            frame = generate_device(cfg, frames=1, t0=t)[0]
+            fmax = max(fmax, float(frame.abs().max()))
+            outs = []
+            for pl, pipe in zip(plans, pipes):
+                outs.append(pipe.process_frame_device(frame[pl.lo:pl.a1]))
+            if outs[0] is None:
+                continue
+            # stitch the velocity field and the residual of every crop from the strips
+            for (y0, x0) in crops:
+                idx = np.zeros((n, n, 2), np.uint8)
+                res = np.zeros((n, n), np.float32)
+                for pl, o in zip(plans, outs):
+                    a, b = max(y0, pl.a0), min(y0 + n, pl.a1)
+                    if a >= b:
+                        continue
+                    idx[a - y0:b - y0] = o.velocity.indices[a - pl.lo:b - pl.lo, x0:x0 + n]
+                    # outputs of anchors [a, b) are rows [a - mhy, b - mhy), held by this strip
+                    res[a - y0:b - y0] = o.residual[a - mhy - pl.lo:b - mhy - pl.lo, x0 - mhx:x0 - mhx + n]
+                gpu_idx[(y0, x0)].append(idx)
+                gpu_res[(y0, x0)].append(res)
+            del frame
+    finally:
+        for p_ in pipes:
+            p_.close()
+    torch.cuda.empty_cache()
+    for (y0, x0) in crops:
+        oy, ox = max(0, y0 - (my - 1)), x0 - (mx - 1)
+        st = _Stats(f"C4 4096x4096 8 strips, crop 256x256 @ ({y0},{x0}), 200 frames")
+        k = 0
+        with _oracle(params, x0 + n - ox, y0 + n - oy) as orc:
+            for t in range(T):
+                crop = generate_device(cfg, frames=1, t0=t, rows=(oy, y0 + n), cols=(ox, x0 + n))[0].cpu().numpy()
+                r = orc.process_frame(crop)
+                if r is None:
+                    continue
+                gi = gpu_idx[(y0, x0)][k]
+                ri = r["indices"][y0 - oy:, x0 - ox:]
+                rres = r["residual"][y0 - oy - mhy:y0 - oy - mhy + n, x0 - ox - mhx:x0 - ox - mhx + n]
+                # the top-edge crop has anchors above My-1 whose outputs are invalid
+                valid = np.ones((n, n), bool)
+                valid[: max(0, (my - 1) - y0)] = False
+                st.add(np.where(valid[..., None], gi, ri), ri, gpu_res[(y0, x0)][k], rres, valid, fmax)
+                k += 1
+        assert k == T - (params.mz - 1)
+        st.done()
