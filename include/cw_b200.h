@@ -32,7 +32,7 @@ enum cw_status {
     CW_ERR_VALUE = -2,     /* maps to ValueError */
     CW_ERR_CUDA = -3,      /* CUDA runtime failure (no CPU fallback exists) */
     CW_ERR_NOMEM = -4,     /* device allocation failed */
-    CW_ERR_UNSUPPORTED = -5 /* geometry without a compiled kernel instance */
+    CW_ERR_UNSUPPORTED = -5 /* request outside the device path's limits (e.g. > 65535 lags) */
 };
 
 /* FilterParams (params.py:34-63); lags as float64 like the reference. */
@@ -163,6 +163,15 @@ int cw_next_frame_slot(cw_handle *h, float **slot);
 int cw_push_inplace(cw_handle *h, int32_t *ready, int64_t *frame_index, void *stream);
 
 int64_t cw_frames_seen(const cw_handle *h);
+
+/* Bytes per velocity-index component: 1 (vidx is (H, W, 2) uint8), or 2
+ * when a lag grid has more than 256 entries (vidx is (H, W, 2) uint16). */
+int32_t cw_index_bytes(const cw_handle *h);
+
+/* 1 when the handle runs the runtime-geometry kernels (parameters with no
+ * compiled fused instance: any window / bandwidth / lag grid that
+ * params.py:114-158 accepts), 0 for the fused kernel. */
+int32_t cw_is_generic(const cw_handle *h);
 
 /* Spectrum backend (pipeline.py:139-142): 0 = recursive (sliding DFT +
  * deadbeat observer, default), 1 = naive: every pixel's spectrum evaluated

@@ -35,7 +35,7 @@ EXPORTS = (
     "cw_frames_seen", "cw_read_view", "cw_launch_info", "cw_set_timing",
     "cw_kernel_time", "cw_copy_to_host", "cw_submit", "cw_submit_raw", "cw_wait", "cw_set_detection", "cw_detections",
     "cw_set_backend", "cw_snapshot_size", "cw_snapshot", "cw_restore",
-    "cw_scene_generate", "cw_scene_last_error",
+    "cw_scene_generate", "cw_scene_last_error", "cw_index_bytes", "cw_is_generic",
 )
 
 
@@ -76,7 +76,8 @@ def build(verbose: bool = False, out: str | None = None, dev: bool = False, extr
         base.append("-Xptxas=-v")
     with tempfile.TemporaryDirectory(prefix="cw_build_") as tmp:
         omp = ["-Xcompiler", "-fopenmp"] if openmp else []
-        jobs = [["nvcc", *base, *omp, "-c", "-o", os.path.join(tmp, "cw_api.o"), os.path.join(CSRC, "cw_api.cu")]]
+        jobs = [["nvcc", *base, *omp, "-c", "-o", os.path.join(tmp, "cw_api.o"), os.path.join(CSRC, "cw_api.cu")],
+                ["nvcc", *base, "-c", "-o", os.path.join(tmp, "cw_generic.o"), os.path.join(CSRC, "cw_generic.cu")]]
         for inst in instances(dev):
             defs = [f"-DCW_{k}={v}" for k, v in zip(("IKX", "IKY", "IKZ", "IBX", "IBY", "INL"), inst)]
             obj = os.path.join(tmp, "cw_inst_" + "_".join(map(str, inst)) + ".o")
@@ -152,6 +153,8 @@ def load():
         "cw_next_frame_slot": (ctypes.c_int, [vp, P(vp)]),
         "cw_push_inplace": (ctypes.c_int, [vp, P(i32), P(i64), vp]),
         "cw_frames_seen": (i64, [vp]),
+        "cw_index_bytes": (i32, [vp]),
+        "cw_is_generic": (i32, [vp]),
         "cw_read_view": (ctypes.c_int, [vp, i32, vp, ctypes.c_size_t]),
         "cw_launch_info": (ctypes.c_int, [vp, P(i32), P(i32), P(i32), P(i32)]),
         "cw_set_timing": (ctypes.c_int, [vp, i32]),

@@ -7,6 +7,7 @@
 // per function; there is no CPU compute path: every frame runs on the GPU
 // or the call fails with CW_ERR_CUDA.
 #include "cw_inst.cuh"
+#include "cw_generic.cuh"
 #include "../../include/cw_b200.h"
 
 #ifdef _OPENMP
@@ -15,6 +16,7 @@
 #include <nvtx3/nvToolsExt.h>  // header-only NVTX ranges (visible in nsys / ncu --nvtx)
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -86,6 +88,15 @@ struct cw_handle {
     float *d_state = nullptr, *d_that = nullptr, *d_coef = nullptr, *d_frames = nullptr;
     float *d_res = nullptr, *d_pred = nullptr;  // 2 output sets each
     uint8_t *d_vidx = nullptr;
+    // runtime-geometry path (cw_generic.cuh) for parameters without a
+    // compiled fused instance; velocity indices are uint16 pairs when a lag
+    // grid has more than 256 entries
+    bool generic = false;
+    int idx_bytes = 1;
+    GenTables gt{};
+    void *d_gtab = nullptr;
+    float2 *d_xf = nullptr;
+    int nxf = 0;  // x-stage frames allocated
     int nslots = 0;  // frame ring slots: max(mhat_z + 2, Mz + 1) (async upload spare; naive window)
     bool naive = false;  // spectrum backend: false = recursive (observer), true = naive window DFT
     int naive_grid = 0;
@@ -181,9 +192,8 @@ static int check_params(const cw_params *p, int W, int H, std::string *msg)
         *msg = "smoothing pole must be in (0,1)";
         return CW_ERR_PARAM;
     }
-    if (p->n_lag_x < 1 || p->n_lag_y < 1 || p->n_lag_x > MAXL || p->n_lag_y > MAXL || !p->lag_x || !p->lag_y) {
-        snprintf(buf, sizeof buf, "lag grids must hold 1..%d entries", MAXL);
-        *msg = buf;
+    if (p->n_lag_x < 1 || p->n_lag_y < 1 || p->n_lag_x > 65535 || p->n_lag_y > 65535 || !p->lag_x || !p->lag_y) {
+        *msg = "lag grids must hold 1..65535 entries";
         return CW_ERR_UNSUPPORTED;
     }
     if (W < m[0] || H < m[1]) {
@@ -299,6 +309,120 @@ static void build_tables(cw_handle *h)
     t.nly = h->nly;
 }
 
+// Device tables of the runtime-geometry path (cw_generic.cuh): built in
+// double, stored as float (spectrum.py:65-74, flow.py:87-97, flow.py:147-163,
+// _kernels.py:286-298, design.py:256-274).
+static int build_generic(cw_handle *h, const float *bank, const int64_t *retained, int nret)
+{
+    const double PI = 3.14159265358979323846;
+    const int Mx = h->mx, My = h->my, Mz = h->mz, nlx = h->nlx, nly = h->nly, nl = nlx * nly;
+    const int nb = Mx * My * Mz;
+    const double nbd = (double)nb, norm = 1.0 / std::sqrt(nbd);
+    std::vector<float2> ex(Mx * Mx), ey(My * My), ez(Mz * Mz), w(Mz), az(Mz), axl((size_t)nlx * Mx),
+        ayl((size_t)nly * My), coef((size_t)nl * nret);
+    auto cis = [](double th, double scale) { return make_float2((float)(scale * std::cos(th)), (float)(scale * std::sin(th))); };
+    for (int k = 0; k < Mx; k++)
+        for (int m = 0; m < Mx; m++)
+            ex[k * Mx + m] = cis(2 * PI * (k - h->kx) * m / Mx, 1.0);
+    for (int k = 0; k < My; k++)
+        for (int m = 0; m < My; m++)
+            ey[k * My + m] = cis(2 * PI * (k - h->ky) * m / My, 1.0);
+    for (int k = 0; k < Mz; k++) {
+        for (int m = 0; m < Mz; m++)
+            ez[k * Mz + m] = cis(2 * PI * (k - h->kz) * m / Mz, 1.0);
+        w[k] = cis(2 * PI * (k - h->kz) / Mz, 1.0);
+        az[k] = cis(-2 * PI * (k - h->kz) / Mz, 1.0 / nbd);
+    }
+    for (int l = 0; l < nlx; l++) {
+        const double g = 0.375 / (0.25 + 0.125 * std::cos(2 * PI * h->lag_x[l] / Mx));
+        for (int k = 0; k < Mx; k++)
+            axl[(size_t)l * Mx + k] = cis(-2 * PI * (k - h->kx) * h->lag_x[l] / Mx, g);
+    }
+    for (int l = 0; l < nly; l++) {
+        const double g = 0.375 / (0.25 + 0.125 * std::cos(2 * PI * h->lag_y[l] / My));
+        for (int k = 0; k < My; k++)
+            ayl[(size_t)l * My + k] = cis(-2 * PI * (k - h->ky) * h->lag_y[l] / My, g);
+    }
+    std::vector<int> order(nl);
+    for (int i = 0; i < nl; i++)
+        order[i] = i;
+    auto n2 = [&](int i) { return h->lag_x[i % nlx] * h->lag_x[i % nlx] + h->lag_y[i / nlx] * h->lag_y[i / nlx]; };
+    std::sort(order.begin(), order.end(), [&](int a, int b) {
+        const double na = n2(a), nb2 = n2(b);
+        if (na != nb2)
+            return na < nb2;
+        if (a % nlx != b % nlx)
+            return a % nlx < b % nlx;
+        return a / nlx < b / nlx;
+    });
+    std::vector<uint32_t> rank(nl), rix(nl), riy(nl);
+    for (int rk = 0; rk < nl; rk++) {
+        rank[order[rk]] = rk;
+        rix[rk] = order[rk] % nlx;
+        riy[rk] = order[rk] / nlx;
+    }
+    std::vector<int32_t> ret(nret);
+    for (int j = 0; j < nret; j++) {
+        if (retained[j] < 0 || retained[j] >= nb)
+            return CW_ERR_VALUE;
+        ret[j] = (int32_t)retained[j];
+    }
+    for (size_t i = 0; i < (size_t)nl * nret; i++)
+        coef[i] = make_float2((float)(norm * bank[2 * i]), (float)(norm * bank[2 * i + 1]));
+    // one device block, 16-byte aligned pieces
+    std::vector<unsigned char> blob;
+    std::vector<size_t> off;
+    auto put = [&](const void *src, size_t bytes) {
+        off.push_back(blob.size());
+        blob.insert(blob.end(), (const unsigned char *)src, (const unsigned char *)src + bytes);
+        blob.resize((blob.size() + 15) / 16 * 16);
+    };
+    put(ex.data(), ex.size() * 8);
+    put(ey.data(), ey.size() * 8);
+    put(ez.data(), ez.size() * 8);
+    put(w.data(), w.size() * 8);
+    put(az.data(), az.size() * 8);
+    put(axl.data(), axl.size() * 8);
+    put(ayl.data(), ayl.size() * 8);
+    put(rank.data(), rank.size() * 4);
+    put(rix.data(), rix.size() * 4);
+    put(riy.data(), riy.size() * 4);
+    put(coef.data(), coef.size() * 8);
+    put(ret.data(), ret.size() * 4);
+    CW_CUDA(h, cudaMalloc(&h->d_gtab, blob.size()));
+    CW_CUDA(h, cudaMemcpy(h->d_gtab, blob.data(), blob.size(), cudaMemcpyHostToDevice));
+    const unsigned char *b = static_cast<const unsigned char *>(h->d_gtab);
+    GenTables &t = h->gt;
+    t.ex = reinterpret_cast<const float2 *>(b + off[0]);
+    t.ey = reinterpret_cast<const float2 *>(b + off[1]);
+    t.ez = reinterpret_cast<const float2 *>(b + off[2]);
+    t.w = reinterpret_cast<const float2 *>(b + off[3]);
+    t.az = reinterpret_cast<const float2 *>(b + off[4]);
+    t.axl = reinterpret_cast<const float2 *>(b + off[5]);
+    t.ayl = reinterpret_cast<const float2 *>(b + off[6]);
+    t.rank = reinterpret_cast<const uint32_t *>(b + off[7]);
+    t.rix = reinterpret_cast<const uint32_t *>(b + off[8]);
+    t.riy = reinterpret_cast<const uint32_t *>(b + off[9]);
+    t.coef = reinterpret_cast<const float2 *>(b + off[10]);
+    t.ret = reinterpret_cast<const int32_t *>(b + off[11]);
+    return CW_OK;
+}
+
+// x-stage planes for nf frames (1: recursive backend, Mz: naive)
+static int ensure_xf(cw_handle *h, int nf)
+{
+    if (h->nxf >= nf)
+        return CW_OK;
+    cudaFree(h->d_xf);
+    h->d_xf = nullptr;
+    h->nxf = 0;
+    const size_t bytes = (size_t)nf * h->mx * h->W * h->H * sizeof(float2);
+    CW_CUDA(h, cudaMalloc(&h->d_xf, bytes));
+    CW_CUDA(h, cudaMemset(h->d_xf, 0, bytes));
+    h->nxf = nf;
+    return CW_OK;
+}
+
 // PEF coefficients on the stored half space (pipeline.py:269-282,
 // _kernels.py:330-342): pred = Re sum_k c(k) S(k) over the retained band,
 // folded so that the kernel computes sum_j coef[j] * z+[j] with
@@ -405,13 +529,13 @@ int cw_create(const cw_params *p, int32_t width, int32_t height, int32_t device,
     const int nl_sym = (p->n_lag_x == p->n_lag_y && sym(p->lag_x, p->n_lag_x) && sym(p->lag_y, p->n_lag_y))
                            ? p->n_lag_x
                            : 0;
-    LaunchFn fn;
-    if (!find_inst(p->kx, p->ky, p->kz, p->bx, p->by, nl_sym, &fn)) {
-        char buf[200];
-        snprintf(buf, sizeof buf, "no compiled kernel for (kx,ky,kz,bx,by)=(%d,%d,%d,%d,%d)", p->kx, p->ky, p->kz,
-                 p->bx, p->by);
-        return fail(nullptr, CW_ERR_UNSUPPORTED, buf);
-    }
+    // the fused kernel when a compiled instance covers the geometry and the
+    // lag grids fit its tables; the runtime-geometry path otherwise (or when
+    // CW_FORCE_GENERIC=1, for testing it on the compiled geometries)
+    LaunchFn fn{};
+    const char *force = std::getenv("CW_FORCE_GENERIC");
+    const bool generic = (force && force[0] == '1') || p->n_lag_x > MAXL || p->n_lag_y > MAXL ||
+                         !find_inst(p->kx, p->ky, p->kz, p->bx, p->by, nl_sym, &fn);
     const int nret_expect = (2 * p->kz + 1) * (2 * p->bx + 1) * (2 * p->by + 1);
     if (n_retained != nret_expect || !bank_c64 || !retained)
         return fail(nullptr, CW_ERR_VALUE, "bank does not match the retained band of these parameters");
@@ -442,17 +566,21 @@ int cw_create(const cw_params *p, int32_t width, int32_t height, int32_t device,
     h->lag_x.assign(p->lag_x, p->lag_x + p->n_lag_x);
     h->lag_y.assign(p->lag_y, p->lag_y + p->n_lag_y);
     h->fn = fn;
-    g_phase_clocks = fn.phase_clocks;
-    build_tables(h);
+    h->generic = generic;
+    h->idx_bytes = (h->nlx > 256 || h->nly > 256) ? 2 : 1;
     std::vector<float> coef;
-    rc = build_coef(h, bank_c64, retained, n_retained, &coef);
-    if (rc != CW_OK) {
-        delete h;
-        return fail(nullptr, rc, "bank/retained layout inconsistent with the parameters");
-    }
-    if (coef.size() != (size_t)h->nlx * h->nly * 2 * fn.retp) {  // host layout == kernel's padded rows
-        delete h;
-        return fail(nullptr, CW_ERR_UNSUPPORTED, "PEF coefficient layout does not match the kernel instance");
+    if (!generic) {
+        g_phase_clocks = fn.phase_clocks;
+        build_tables(h);
+        rc = build_coef(h, bank_c64, retained, n_retained, &coef);
+        if (rc != CW_OK) {
+            delete h;
+            return fail(nullptr, rc, "bank/retained layout inconsistent with the parameters");
+        }
+        if (coef.size() != (size_t)h->nlx * h->nly * 2 * fn.retp) {  // host layout == kernel's padded rows
+            delete h;
+            return fail(nullptr, CW_ERR_UNSUPPORTED, "PEF coefficient layout does not match the kernel instance");
+        }
     }
 
     auto cleanup_fail = [&](int code, const std::string &m) {
@@ -465,27 +593,36 @@ int cw_create(const cw_params *p, int32_t width, int32_t height, int32_t device,
         return cleanup_fail(CW_ERR_CUDA, "cudaSetDevice failed (no CUDA device?)");
     if (cudaStreamCreateWithFlags(&h->own, cudaStreamNonBlocking) != cudaSuccess)
         return cleanup_fail(CW_ERR_CUDA, "cudaStreamCreate failed");
-    if (cudaFuncSetAttribute(fn.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fn.smem) != cudaSuccess)
-        return cleanup_fail(CW_ERR_CUDA, "cannot reserve shared memory for the frame kernel");
     int occ = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn.kernel, fn.threads, fn.smem);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    if (occ < 1 || sms < 1)
-        return cleanup_fail(CW_ERR_CUDA, "frame kernel cannot be resident on this device");
-    const long long units = (long long)h->NXB * (height - halo_rows);
-    h->grid = (int)std::min<long long>((long long)occ * sms, std::max<long long>(1, units / 2));
-    h->sms = sms;
+    if (!generic) {
+        if (cudaFuncSetAttribute(fn.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fn.smem) != cudaSuccess)
+            return cleanup_fail(CW_ERR_CUDA, "cannot reserve shared memory for the frame kernel");
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn.kernel, fn.threads, fn.smem);
+        if (occ < 1 || sms < 1)
+            return cleanup_fail(CW_ERR_CUDA, "frame kernel cannot be resident on this device");
+        const long long units = (long long)h->NXB * (height - halo_rows);
+        h->grid = (int)std::min<long long>((long long)occ * sms, std::max<long long>(1, units / 2));
+    }
+    h->sms = std::max(1, sms);
 
     const size_t pix_packets = (size_t)height * h->NXB;
-    h->state_floats = pix_packets * fn.nsp * 32 * 2;
-    h->that_floats = pix_packets * fn.ntp * 32 * 2;
     const size_t HW = (size_t)width * height;
+    if (generic) {  // [plane][pixel] float2: full spectrum z+, T^ (My x Mx)
+        h->state_floats = HW * h->mx * h->my * h->mz * 2;
+        h->that_floats = HW * h->mx * h->my * 2;
+        if (build_generic(h, bank_c64, retained, n_retained) != CW_OK || ensure_xf(h, 1) != CW_OK)
+            return cleanup_fail(CW_ERR_NOMEM, "runtime-geometry tables / buffers: " + h->err);
+    } else {
+        h->state_floats = pix_packets * fn.nsp * 32 * 2;
+        h->that_floats = pix_packets * fn.ntp * 32 * 2;
+    }
     if (cudaMalloc(&h->d_state, h->state_floats * 4) != cudaSuccess ||
         cudaMalloc(&h->d_that, h->that_floats * 4) != cudaSuccess ||
-        cudaMalloc(&h->d_coef, coef.size() * 4) != cudaSuccess ||
+        (!generic && cudaMalloc(&h->d_coef, coef.size() * 4) != cudaSuccess) ||
         cudaMalloc(&h->d_frames, HW * 4 * std::max(h->mhz + 2, h->mz + 1)) != cudaSuccess ||
         cudaMalloc(&h->d_res, HW * 4 * 2) != cudaSuccess || cudaMalloc(&h->d_pred, HW * 4 * 2) != cudaSuccess ||
-        cudaMalloc(&h->d_vidx, HW * 2 * 2) != cudaSuccess)
+        cudaMalloc(&h->d_vidx, HW * 2 * 2 * h->idx_bytes) != cudaSuccess)
         return cleanup_fail(CW_ERR_NOMEM, "device allocation failed");
     cudaMemsetAsync(h->d_state, 0, h->state_floats * 4, h->own);
     cudaMemsetAsync(h->d_that, 0, h->that_floats * 4, h->own);
@@ -493,7 +630,7 @@ int cw_create(const cw_params *p, int32_t width, int32_t height, int32_t device,
     cudaMemsetAsync(h->d_frames, 0, HW * 4 * h->nslots, h->own);
     cudaMemsetAsync(h->d_res, 0, HW * 4 * 2, h->own);
     cudaMemsetAsync(h->d_pred, 0, HW * 4 * 2, h->own);
-    cudaMemsetAsync(h->d_vidx, 0, HW * 2 * 2, h->own);
+    cudaMemsetAsync(h->d_vidx, 0, HW * 2 * 2 * h->idx_bytes, h->own);
     if (cudaStreamCreateWithFlags(&h->up, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&h->down, cudaStreamNonBlocking) != cudaSuccess)
         return cleanup_fail(CW_ERR_CUDA, "cudaStreamCreate failed");
@@ -502,7 +639,8 @@ int cw_create(const cw_params *p, int32_t width, int32_t height, int32_t device,
             cudaEventCreateWithFlags(&h->ev_k[i], cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&h->ev_down[i], cudaEventDisableTiming) != cudaSuccess)
             return cleanup_fail(CW_ERR_CUDA, "cudaEventCreate failed");
-    cudaMemcpyAsync(h->d_coef, coef.data(), coef.size() * 4, cudaMemcpyHostToDevice, h->own);
+    if (!generic)
+        cudaMemcpyAsync(h->d_coef, coef.data(), coef.size() * 4, cudaMemcpyHostToDevice, h->own);
     if (cudaStreamSynchronize(h->own) != cudaSuccess)
         return cleanup_fail(CW_ERR_CUDA, "device initialisation failed");
     *out = h;
@@ -524,6 +662,8 @@ void cw_destroy(cw_handle *h)
     cudaFree(h->d_res);
     cudaFree(h->d_pred);
     cudaFree(h->d_vidx);
+    cudaFree(h->d_gtab);
+    cudaFree(h->d_xf);
     cudaFree(h->d_det);
     if (h->h_det)
         cudaFreeHost(h->h_det);
@@ -570,6 +710,10 @@ int cw_set_forced_velocity(cw_handle *h, int32_t ix, int32_t iy)
 
 int64_t cw_frames_seen(const cw_handle *h) { return h ? h->frames_seen : -1; }
 
+int32_t cw_index_bytes(const cw_handle *h) { return h ? h->idx_bytes : -1; }
+
+int32_t cw_is_generic(const cw_handle *h) { return h ? (h->generic ? 1 : 0) : -1; }
+
 int cw_next_frame_slot(cw_handle *h, float **slot)
 {
     if (!h || !slot)
@@ -609,7 +753,7 @@ static int run_frame(cw_handle *h, cudaStream_t s, int32_t *ready, int64_t *fram
     const size_t set = (size_t)(n & 1);  // double-buffered outputs
     a.res = res_o ? res_o : h->d_res + set * HW;
     a.pred = pred_o ? pred_o : h->d_pred + set * HW;
-    a.vidx = vidx_o ? vidx_o : h->d_vidx + set * HW * 2;
+    a.vidx = vidx_o ? vidx_o : h->d_vidx + set * HW * 2 * h->idx_bytes;
     a.W = h->W;
     a.H = h->H;
     a.NXB = h->NXB;
@@ -640,7 +784,49 @@ static int run_frame(cw_handle *h, cudaStream_t s, int32_t *ready, int64_t *fram
         h->ev_used += 2;
         CW_CUDA(h, cudaEventRecord(e0, s));
     }
-    if (h->naive && rd) {
+    if (h->generic) {
+        GenArgs g;
+        g.frames = h->d_frames;
+        g.nslots = h->nslots;
+        g.n = n;
+        g.delayed = a.delayed;
+        g.xf = h->d_xf;
+        g.state = reinterpret_cast<float2 *>(h->d_state);
+        g.that = reinterpret_cast<float2 *>(h->d_that);
+        g.res = a.res;
+        g.pred = a.pred;
+        g.vidx = a.vidx;
+        g.idx16 = h->idx_bytes == 2;
+        g.W = h->W;
+        g.H = h->H;
+        g.NXB = h->NXB;
+        g.y_begin = h->halo;
+        g.y_off = h->row_off;
+        g.kx = h->kx;
+        g.ky = h->ky;
+        g.kz = h->kz;
+        g.mx = h->mx;
+        g.my = h->my;
+        g.mz = h->mz;
+        g.nb = h->mx * h->my * h->mz;
+        g.nlx = h->nlx;
+        g.nly = h->nly;
+        g.nc = (2 * h->kz + 1) * (2 * h->bx + 1) * (2 * h->by + 1);
+        g.mhx = h->mhx;
+        g.mhy = h->mhy;
+        g.ready = rd;
+        g.first = a.first;
+        g.naive = h->naive;
+        g.forced_ix = h->forced_ix;
+        g.forced_iy = h->forced_iy;
+        g.alpha = (float)h->alpha;
+        g.beta = (float)(1.0 - h->alpha);
+        g.inv_mz = (float)(1.0 / h->mz);
+        g.det = a.det;
+        g.det_tau = a.det_tau;
+        g.det_cap = a.det_cap;
+        CW_CUDA(h, gen_launch(g, h->gt, h->sms, s));
+    } else if (h->naive && rd) {
         // non-recursive spectrum of frames n-Mz+1 .. n into the state packets
         NaiveArgs na;
         na.frames = h->d_frames;
@@ -655,8 +841,10 @@ static int run_frame(cw_handle *h, cudaStream_t s, int32_t *ready, int64_t *fram
         h->fn.launch_naive(na, h->tab, h->naive_grid, s);
         CW_CUDA(h, cudaGetLastError());
     }
-    h->fn.launch(a, h->tab, h->grid, s);
-    CW_CUDA(h, cudaGetLastError());
+    if (!h->generic) {
+        h->fn.launch(a, h->tab, h->grid, s);
+        CW_CUDA(h, cudaGetLastError());
+    }
     if (h->timing)
         CW_CUDA(h, cudaEventRecord(e1, s));
     if (a.det) {  // results to the pinned mirror of this frame (ordered on s)
@@ -830,7 +1018,7 @@ int cw_push(cw_handle *h, const float *frame, float *residual, float *prediction
             sync = true;
         }
         if (vidx) {
-            CW_CUDA(h, cudaMemcpyAsync(vidx, h->d_vidx + set * HW * 2, HW * 2, cudaMemcpyDeviceToHost, s));
+            CW_CUDA(h, cudaMemcpyAsync(vidx, h->d_vidx + set * HW * 2 * h->idx_bytes, HW * 2 * h->idx_bytes, cudaMemcpyDeviceToHost, s));
             sync = true;
         }
     }
@@ -850,7 +1038,7 @@ int cw_device_outputs(cw_handle *h, float **residual, float **prediction, uint8_
     if (prediction)
         *prediction = h->d_pred + set * HW;
     if (vidx)
-        *vidx = h->d_vidx + set * HW * 2;
+        *vidx = h->d_vidx + set * HW * 2 * h->idx_bytes;
     return CW_OK;
 }
 
@@ -953,7 +1141,7 @@ static int submit_impl(cw_handle *h, const void *samples, int format, double sca
         if (prediction)
             CW_CUDA(h, cudaMemcpyAsync(prediction, h->d_pred + set * HW, HW * 4, cudaMemcpyDeviceToHost, h->down));
         if (vidx)
-            CW_CUDA(h, cudaMemcpyAsync(vidx, h->d_vidx + set * HW * 2, HW * 2, cudaMemcpyDeviceToHost, h->down));
+            CW_CUDA(h, cudaMemcpyAsync(vidx, h->d_vidx + set * HW * 2 * h->idx_bytes, HW * 2 * h->idx_bytes, cudaMemcpyDeviceToHost, h->down));
     }
     CW_CUDA(h, cudaEventRecord(h->ev_down[e], h->down));
     h->ready_of[e] = rd;
@@ -1134,13 +1322,13 @@ int cw_launch_info(const cw_handle *h, int32_t *kernels_per_push, int32_t *grid,
     if (!h)
         return CW_ERR_VALUE;
     if (kernels_per_push)
-        *kernels_per_push = 1;
+        *kernels_per_push = h->generic ? 3 : 1;
     if (grid)
-        *grid = h->grid;
+        *grid = h->generic ? 0 : h->grid;
     if (block)
-        *block = h->fn.threads;
+        *block = h->generic ? 128 : h->fn.threads;
     if (smem_bytes)
-        *smem_bytes = (int32_t)h->fn.smem;
+        *smem_bytes = h->generic ? 0 : (int32_t)h->fn.smem;
     return CW_OK;
 }
 
@@ -1149,6 +1337,12 @@ int cw_set_backend(cw_handle *h, int32_t naive)
     DeviceGuard dg(h);
     if (!h)
         return CW_ERR_VALUE;
+    if (h->generic) {
+        if (naive && ensure_xf(h, h->mz) != CW_OK)
+            return CW_ERR_NOMEM;
+        h->naive = naive != 0;
+        return CW_OK;
+    }
     if (naive && !h->naive_grid) {
         CW_CUDA(h, cudaSetDevice(h->device));
         CW_CUDA(h, cudaFuncSetAttribute(h->fn.naive_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1204,6 +1398,24 @@ int cw_read_view(cw_handle *h, int32_t what, void *dst, size_t bytes)
         if (bytes != h->state_floats * 4)
             return fail(h, CW_ERR_VALUE, "view size mismatch");
         CW_CUDA(h, cudaMemcpy(dst, h->d_state, bytes, cudaMemcpyDeviceToHost));
+        return CW_OK;
+    }
+    if (h->generic && (what == 0 || what == 1)) {
+        // planes [plane][pixel] of the full spectrum: state = z+, S = norm z+;
+        // T^ planes (My, Mx) -- transposed into the reference layouts
+        const size_t HW = (size_t)W * H, np = what == 0 ? (size_t)Mx * My * Mz : (size_t)Mx * My;
+        if (bytes != HW * np * 16)
+            return fail(h, CW_ERR_VALUE, "view size mismatch");
+        std::vector<float2> pl(HW * np);
+        CW_CUDA(h, cudaMemcpy(pl.data(), what == 0 ? h->d_state : h->d_that, pl.size() * 8, cudaMemcpyDeviceToHost));
+        const double sc = what == 0 ? 1.0 / std::sqrt((double)Mx * My * Mz) : 1.0;
+        double *o = static_cast<double *>(dst);
+        for (size_t q = 0; q < np; q++)
+            for (size_t px = 0; px < HW; px++) {
+                const float2 v = pl[q * HW + px];
+                o[2 * (px * np + q)] = sc * v.x;
+                o[2 * (px * np + q) + 1] = sc * v.y;
+            }
         return CW_OK;
     }
     // pair j of pixel (y, x) in a packet buffer of `np` pairs per pixel

@@ -77,17 +77,18 @@ def apply_pef(bins, kernel, delayed_intensity: float):
 
 class _LazyVelocityField(VelocityField):
     """VelocityField whose int32 ``indices`` and float64 ``velocities``
-    (flow.py:134-144) are expanded from the device's uint8 (ix, iy) pairs on
-    first access, through 64K-entry lookup tables."""
+    (flow.py:134-144) are expanded from the device's (ix, iy) pairs on first
+    access (uint8 pairs through 64K-entry lookup tables; uint16 pairs for
+    lag grids longer than 256 directly)."""
 
-    def __init__(self, codes, lut_i, lut_v):
-        self._codes, self._lut_i, self._lut_v = codes, lut_i, lut_v
+    def __init__(self, vidx, pipe):
+        self._vidx, self._pipe = vidx, pipe
         self._i = self._v = None
 
     @property
     def indices(self):
         if self._i is None:
-            self._i = self._lut_i[self._codes]
+            self._i = self._pipe._indices_of(self._vidx)
         return self._i
 
     @indices.setter
@@ -97,7 +98,7 @@ class _LazyVelocityField(VelocityField):
     @property
     def velocities(self):
         if self._v is None:
-            self._v = self._lut_v[self._codes]
+            self._v = self._pipe._velocities_of(self._vidx)
         return self._v
 
     @velocities.setter
@@ -126,31 +127,32 @@ class _PinnedPool:
         self._lock = threading.RLock()
         self._outstanding = 0
 
-    def take_outputs(self, h, w):
+    def take_outputs(self, h, w, idx_bytes=1):
         """(residual, prediction, velocity-index) arrays of one call, carved
         from a single pinned block (one allocation / finalizer per call; the
         block returns to the pool when the last of the three is collected)."""
         import torch
 
-        key = ("outputs", h, w)
+        key = ("outputs", h, w, idx_bytes)
         hw = h * w
+        nbytes = (8 + 2 * idx_bytes) * hw
         with self._lock:
-            if self._outstanding + 10 * hw > self.MAX_OUTSTANDING_BYTES and self._outstanding > 0:
+            if self._outstanding + nbytes > self.MAX_OUTSTANDING_BYTES and self._outstanding > 0:
                 tensor = False  # pool exhausted: pageable arrays (the device copies through staging)
             else:
                 stack = self._free.setdefault(key, [])
                 tensor = stack.pop() if stack else None
-                self._outstanding += 10 * hw
+                self._outstanding += nbytes
         if tensor is False:
-            blk = np.empty(10 * hw, np.uint8)
+            blk = np.empty(nbytes, np.uint8)
         else:
             if tensor is None:
-                tensor = torch.empty(10 * hw, dtype=torch.uint8, pin_memory=True)
+                tensor = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
             blk = tensor.numpy()
-            weakref.finalize(blk, self._give, key, tensor, 10 * hw)
+            weakref.finalize(blk, self._give, key, tensor, nbytes)
         res = blk[: 4 * hw].view(np.float32).reshape(h, w)
         pred = blk[4 * hw : 8 * hw].view(np.float32).reshape(h, w)
-        vidx = blk[8 * hw :].reshape(h, w, 2)
+        vidx = blk[8 * hw :].view(np.uint8 if idx_bytes == 1 else np.uint16).reshape(h, w, 2)
         return res, pred, vidx
 
     def _give(self, key, tensor, nbytes):
@@ -228,7 +230,7 @@ class Pipeline:
         self._lag_x = np.asarray(params.lag_grid_x, dtype=np.float64)
         self._lag_y = np.asarray(params.lag_grid_y, dtype=np.float64)
         # (ix | iy << 8) -> (ix, iy) int32 and (vx, vy) float64
-        code = np.arange(65536)
+        code = np.arange(65536)  # (used for grids of <= 256 lags, i.e. uint8 index pairs)
         ix, iy = np.minimum(code & 255, len(self._lag_x) - 1), np.minimum(code >> 8, len(self._lag_y) - 1)
         self._lut_i = np.stack([code & 255, code >> 8], axis=-1).astype(np.int32)
         self._lut_v = np.stack([self._lag_x[ix], self._lag_y[iy]], axis=-1)
@@ -256,6 +258,7 @@ class Pipeline:
         )
         _native.check(rc, None)
         self._h = handle
+        self._idx_bytes = int(lib.cw_index_bytes(self._h))
         if self._forced is not None:
             _native.check(lib.cw_set_forced_velocity(self._h, *self._forced), self._h)
         if spectrum_backend == "naive":
@@ -297,7 +300,7 @@ class Pipeline:
         lib = _native.load()
         t0 = time.perf_counter()
         h, w = self.height, self.width
-        res, pred, vidx = self._pool.take_outputs(h, w)
+        res, pred, vidx = self._pool.take_outputs(h, w, self._idx_bytes)
         ready = ctypes.c_int32(0)
         fidx = ctypes.c_int64(-1)
         rc = lib.cw_push(self._h, frame.ctypes.data, res.ctypes.data, pred.ctypes.data, vidx.ctypes.data,
@@ -382,7 +385,7 @@ class Pipeline:
                 frame = np.ascontiguousarray(frame, dtype=">u2" if pgm else np.float32)
                 if frame.shape != (h, w):
                     raise ValueError(f"frame shape {frame.shape} != {(h, w)}")
-                res, pred, vidx = self._pool.take_outputs(h, w)
+                res, pred, vidx = self._pool.take_outputs(h, w, self._idx_bytes)
                 ticket = ctypes.c_int64(-1)
                 rc = lib.cw_submit_raw(self._h, frame.ctypes.data, _native.FMT_PGM16 if pgm else _native.FMT_F32LE,
                                        float(scale), float(offset), res.ctypes.data, pred.ctypes.data,
@@ -441,7 +444,7 @@ class Pipeline:
         h, w = self.height, self.width
         res = np.empty((h, w), np.float32)
         pred = np.empty((h, w), np.float32)
-        vidx = np.empty((h, w, 2), np.uint8)
+        vidx = np.empty((h, w, 2), np.uint8 if self._idx_bytes == 1 else np.uint16)
         for dst, src in ((res, res_p), (pred, pred_p), (vidx, vidx_p)):
             _native.check(lib.cw_copy_to_host(self._h, dst.ctypes.data, src, dst.nbytes), self._h)
         self._set_timings(time.perf_counter() - t0, True)
@@ -450,10 +453,23 @@ class Pipeline:
             out.imag_peak = self._imag_peak_from_state(vidx)
         return out
 
+    def _indices_of(self, vidx) -> np.ndarray:
+        """(H, W, 2) int32 [ix, iy] from the device's index pairs."""
+        if self._idx_bytes == 1:
+            return self._lut_i[vidx.view(np.uint16).reshape(vidx.shape[:2])]
+        return vidx.astype(np.int32)
+
+    def _velocities_of(self, vidx, dtype=np.float64) -> np.ndarray:
+        """(H, W, 2) [vx, vy] lags of the device's index pairs (float64 as
+        flow.VelocityField; ``dtype`` float32 for velocity files)."""
+        if self._idx_bytes == 1:
+            lut = self._lut_v if dtype == np.float64 else self._lut_v.astype(dtype)
+            return np.take(lut, vidx.view(np.uint16).reshape(vidx.shape[:2]), axis=0)
+        return np.stack([self._lag_x[vidx[..., 0]], self._lag_y[vidx[..., 1]]], axis=-1).astype(dtype)
+
     def _wrap(self, frame_index, res, pred, vidx, ticket=None) -> WhitenedOutput:
-        codes = vidx.view(np.uint16).reshape(vidx.shape[:2])
         out = WhitenedOutput(frame_index=frame_index, residual=res, prediction=pred,
-                             velocity=_LazyVelocityField(codes, self._lut_i, self._lut_v),
+                             velocity=_LazyVelocityField(vidx, self),
                              mask=self.mask, imag_peak=0.0 if self._hermitian else float("nan"))
         if self._detect and ticket is not None:
             out.detections, out.metrics = self._fetch_detections(ticket)

@@ -185,7 +185,8 @@ def _stream(reader: SequenceReader, pipe: Pipeline, consume, *, want_pred: bool,
     for _ in range(n_out):
         free_out.put((_pinned(h * w * 4).view(np.float32).reshape(h, w),
                       _pinned(h * w * 4).view(np.float32).reshape(h, w),
-                      _pinned(h * w * 2).reshape(h, w, 2)))
+                      _pinned(h * w * 2 * pipe._idx_bytes).view(np.uint8 if pipe._idx_bytes == 1 else np.uint16)
+                      .reshape(h, w, 2)))
     ready_in: queue.Queue = queue.Queue(maxsize=n_in)
     to_write: queue.Queue = queue.Queue(maxsize=n_out)
     errors: list[BaseException] = []
@@ -298,7 +299,6 @@ def filter_sequence(input_dir, out_dir, params: FilterParams | None = None, *, d
         first_index = [None]
         with Pipeline(params, w, h, spectrum_backend=spectrum_backend, device=device,
                       detect_threshold=0.0 if want_metrics else None, max_detections=0) as pipe:
-            lut_v = pipe._lut_v.astype("<f4")  # (ix | iy << 8) -> (vx, vy), f64 lags rounded to f32
 
             def consume(fidx, _t, res, pred, vidx, stats):
                 if first_index[0] is None:
@@ -306,13 +306,12 @@ def filter_sequence(input_dir, out_dir, params: FilterParams | None = None, *, d
                 res_w.append(res)
                 if pred_w is not None:
                     pred_w.append(pred)
-                codes = vidx.view(np.uint16).reshape(h, w)
-                if vel_fh is not None:
-                    vel_fh.write(np.take(lut_v, codes, axis=0).data)
+                if vel_fh is not None:  # f64 lags rounded to f32
+                    vel_fh.write(pipe._velocities_of(vidx, np.dtype("<f4")).data)
                 if want_metrics:
                     # metrics from the float64 lags, as cli.compute_metrics_row
                     velocity = (None if truth is None
-                                else SimpleNamespace(velocities=np.take(pipe._lut_v, codes, axis=0)))
+                                else SimpleNamespace(velocities=pipe._velocities_of(vidx)))
                     rows.append(metrics_row(_Out(fidx, res, pipe.mask, velocity, stats), params, truth))
 
             try:
@@ -371,10 +370,8 @@ def flow_sequence(input_dir, out_dir, params: FilterParams | None = None, *, fmt
         first, count = [None], [0]
         ys, xs = np.mgrid[params.my - 1:h, params.mx - 1:w]
         with Pipeline(params, w, h, device=device) as pipe:
-            lut_v = pipe._lut_v.astype("<f4")
-
             def consume(_fidx, t_in, _res, _pred, vidx, _stats):
-                vel = np.take(lut_v, vidx.view(np.uint16).reshape(h, w), axis=0)
+                vel = pipe._velocities_of(vidx, np.dtype("<f4"))
                 if first[0] is None:
                     first[0] = t_in
                 count[0] += 1

@@ -1,0 +1,214 @@
+"""Every validate-legal FilterParams runs on the device (params.py:114-158;
+SPEC.md:69 makes the geometry runtime configuration).
+
+Parameters with a compiled fused instance run the fused kernel; every
+other legal set -- any half window / bandwidth, asymmetric windows, any lag
+grid (odd or even, asymmetric, more than 33 or more than 256 entries) --
+runs the runtime-geometry kernels (csrc/cw_generic.cu).  Both are checked
+against the float64 oracle / the reference's golden vectors with the
+tolerances of tests/parity.py.  CW_FORCE_GENERIC=1 routes the compiled
+geometries through the runtime-geometry path too, so the two device paths
+are also compared with each other."""
+
+import numpy as np
+import pytest
+
+from conftest import SMALL_CASES, small_case
+from parity import RES_TOL, VEL_FRAC, agreeing_outputs, residual_error, velocity_agreement
+
+pytestmark = pytest.mark.gpu
+
+
+def _frames(t, h, w, seed=0, vx=1.25, vy=0.5):
+    rng = np.random.default_rng(seed)
+    xs, ys = np.arange(w)[None, :], np.arange(h)[:, None]
+    return np.stack([
+        10.0 + 0.3 * np.cos(2 * np.pi * ((xs - vx * n) / 9.0 + (ys - vy * n) / 7.0))
+        + 0.2 * np.cos(2 * np.pi * ((xs - vx * n) / 13.0 - (ys - vy * n) / 11.0))
+        + 0.05 * rng.standard_normal((h, w)) for n in range(t)
+    ]).astype(np.float32)
+
+
+def _check(params, frames, gpu_outs, ref_outs):
+    assert len(gpu_outs) == len(ref_outs) > 0
+    fmax = float(np.abs(frames).max())
+    for g, r in zip(gpu_outs, ref_outs):
+        assert g.frame_index == r["frame_index"]
+        assert velocity_agreement(g.velocity.indices, r["indices"], params) >= VEL_FRAC
+        m = g.mask & agreeing_outputs(g.velocity.indices, r["indices"], params)
+        if m.any():
+            assert residual_error(g.residual, r["residual"], m, fmax) <= RES_TOL
+        assert np.all(g.residual[~g.mask] == 0)
+
+
+def _run(params, frames, **kw):
+    from paper_1408_3526_b200 import Pipeline, _native
+
+    t, h, w = frames.shape
+    with Pipeline(params, w, h, **kw) as pipe:
+        outs = [o for o in map(pipe.process_frame, frames) if o is not None]
+        generic = bool(_native.load().cw_is_generic(pipe._h))
+    return outs, generic
+
+
+def _oracle(params, frames, forced=None):
+    from oracle.oracle import OraclePipeline
+
+    t, h, w = frames.shape
+    with OraclePipeline(params, w, h, forced_velocity=forced) as orc:
+        return [o for o in map(orc.process_frame, frames) if o is not None]
+
+
+@pytest.mark.parametrize("name", SMALL_CASES)
+def test_generic_path_on_the_golden_cases(name, monkeypatch):
+    """The reference's own outputs (tests/golden/small_cases.npz) through the
+    runtime-geometry kernels."""
+    monkeypatch.setenv("CW_FORCE_GENERIC", "1")
+    p, frames, forced, want = small_case(name)
+    outs, generic = _run(p, frames, forced_velocity=forced)
+    assert generic
+    ref = [{"frame_index": int(want["frame_index"][k]), "indices": want["indices"][k],
+            "residual": want["residual"][k]} for k in range(len(want["frame_index"]))]
+    _check(p, frames, outs, ref)
+
+
+LEGAL = {
+    # (kx, ky, kz, bx, by, mhat, lag_x, lag_y): none has a compiled instance
+    "bx2": (4, 4, 2, 2, 3, (4, 4, 2), None, None),
+    "kz3": (4, 4, 3, 3, 3, (4, 4, 3), None, None),
+    "ky3_by2": (4, 3, 2, 3, 2, (4, 3, 2), None, None),
+    "k6": (6, 6, 2, 5, 5, (6, 6, 2), None, None),
+    "k1_b0": (1, 1, 1, 0, 0, (1, 1, 1), (-0.5, 0.0, 0.5), (-1.0, 0.0, 1.0)),
+    "k2_mhat0": (2, 3, 1, 1, 2, (0, 1, 0), None, None),
+    "lags41_asym": (4, 4, 2, 3, 3, (4, 4, 2), tuple(-2.0 + 0.1 * i for i in range(41)),
+                    tuple(-1.5 + 0.125 * i for i in range(25))),
+    "lags_even": (4, 4, 2, 3, 3, (4, 4, 2), (-1.5, -0.5, 0.5, 1.5), (-1.0, 0.0, 0.75)),
+}
+
+
+def _params(spec):
+    from paper_1408_3526_b200 import FilterParams, validate
+
+    kx, ky, kz, bx, by, mhat, lx, ly = spec
+    kw = dict(kx=kx, ky=ky, kz=kz, bx=bx, by=by, mhat=mhat)
+    if lx is not None:
+        kw.update(lag_grid_x=lx, lag_grid_y=ly)
+    elif min(kx, ky) < 2:
+        kw.update(lag_grid_x=(-1.0, 0.0, 1.0), lag_grid_y=(-1.0, 0.0, 1.0))
+    p = FilterParams(**kw)
+    validate(p)
+    return p
+
+
+@pytest.mark.parametrize("name", sorted(LEGAL))
+def test_legal_geometry_matches_oracle(name):
+    p = _params(LEGAL[name])
+    h, w = 2 * p.my + 22, 2 * p.mx + 31
+    frames = _frames(p.mz + 7, h, w, seed=len(name))
+    outs, generic = _run(p, frames)
+    # no compiled instance: the runtime-geometry path ran (a short lag grid on
+    # a compiled geometry runs the fused kernel's runtime-loop instance)
+    assert generic == (name != "lags_even")
+    _check(p, frames, outs, _oracle(p, frames))
+
+
+def test_more_than_256_lags_use_16_bit_indices():
+    """A 260-entry lag grid (legal: params.py:142-157 bounds only the span)
+    returns indices > 255: the device writes uint16 pairs."""
+    from paper_1408_3526_b200 import FilterParams
+
+    lx = tuple(float(v) for v in np.linspace(-3.9, 3.9, 260))
+    p = FilterParams(lag_grid_x=lx, lag_grid_y=(-0.5, 0.0, 0.5))
+    frames = _frames(9, 30, 36, seed=9, vx=1.3, vy=0.1)
+    outs, generic = _run(p, frames)
+    assert generic
+    ref = _oracle(p, frames)
+    _check(p, frames, outs, ref)
+    assert max(int(o.velocity.indices[..., 0].max()) for o in outs) > 255
+    v = outs[-1].velocity
+    assert np.array_equal(v.velocities[..., 0], np.asarray(lx)[v.indices[..., 0]])
+
+
+def test_generic_equals_fused_on_the_default_geometry(params, monkeypatch):
+    """Same frames through the fused kernel and (forced) the runtime path."""
+    frames = _frames(12, 70, 90, seed=3)
+    fused, g0 = _run(params, frames)
+    monkeypatch.setenv("CW_FORCE_GENERIC", "1")
+    gen, g1 = _run(params, frames)
+    assert not g0 and g1
+    fmax = float(np.abs(frames).max())
+    for a, b in zip(fused, gen):
+        assert velocity_agreement(a.velocity.indices, b.velocity.indices, params) >= VEL_FRAC
+        m = a.mask & agreeing_outputs(a.velocity.indices, b.velocity.indices, params)
+        assert residual_error(a.residual, b.residual.astype(np.float64), m, fmax) <= RES_TOL
+
+
+def test_generic_naive_backend_forced_velocity_and_detection():
+    """The runtime path's naive spectrum backend, forced velocity and the
+    fused detection metrics (pipeline.py:139-142, 174-177, 260-265)."""
+    p = _params(LEGAL["kz3"])
+    frames = _frames(11, 40, 44, seed=4)
+    ref = _oracle(p, frames)
+    outs, generic = _run(p, frames, spectrum_backend="naive", detect_threshold=0.05)
+    assert generic
+    _check(p, frames, outs, ref)
+    for o in outs:
+        want = np.sqrt(np.mean(o.residual[o.mask].astype(np.float64) ** 2))
+        assert o.metrics["residual_rms"] == pytest.approx(want, rel=1e-12)
+        assert o.metrics["n_valid"] == int(o.mask.sum())
+    forced = (p.lag_grid_x[2], p.lag_grid_y[5])
+    outs, _ = _run(p, frames, forced_velocity=forced)
+    _check(p, frames, outs, _oracle(p, frames, forced=forced))
+    assert np.all(outs[-1].velocity.indices == (2, 5))
+
+
+def test_generic_strips_stitch_to_the_full_frame():
+    """Strip sharding (halo rows + row offset, strips.py) on the runtime path."""
+    import torch
+
+    from paper_1408_3526_b200 import Pipeline
+    from paper_1408_3526_b200.strips import plan_strips
+
+    p = _params(LEGAL["ky3_by2"])
+    frames = _frames(9, 60, 50, seed=6)
+    full, _ = _run(p, frames)
+    for pl in plan_strips(p, 60, 3):
+        with Pipeline(p, 50, pl.local_height, _strip=(pl.halo, pl.lo)) as pipe:
+            k = 0
+            for f in frames:
+                o = pipe.process_frame_device(torch.from_numpy(f[pl.lo:pl.a1]).cuda())
+                if o is None:
+                    continue
+                g = full[k]
+                k += 1
+                assert np.array_equal(o.velocity.indices[pl.halo:], g.velocity.indices[pl.a0:pl.a1])
+                mhy = p.mhat[1]
+                r0 = pl.halo - mhy if pl.halo else 0
+                np.testing.assert_array_equal(o.residual[r0:pl.local_height - mhy],
+                                              g.residual[pl.lo + r0:pl.a1 - mhy])
+
+
+def test_generic_snapshot_and_views(monkeypatch):
+    """Checkpoint / resume and the spectrum / T^ parity views on the runtime
+    path (the spectrum against the oracle's, per pixel)."""
+    from oracle.oracle import OraclePipeline
+    from paper_1408_3526_b200 import Pipeline
+    from parity import SPEC_TOL, per_pixel_rel
+
+    p = _params(LEGAL["bx2"])
+    frames = _frames(10, 30, 34, seed=8)
+    with Pipeline(p, 34, 30) as a, OraclePipeline(p, 34, 30) as orc:
+        for f in frames[:7]:
+            a.process_frame(f)
+            orc.process_frame(f)
+        err = per_pixel_rel(a.spectrum()[p.my - 1:, p.mx - 1:], orc.sbins()[p.my - 1:, p.mx - 1:], axes=(2, 3, 4))
+        assert err <= SPEC_TOL
+        assert a.smoothed_state().shape == (30, 34, p.my, p.mx)
+        snap = a.snapshot()
+        rest_a = [a.process_frame(f) for f in frames[7:]]
+    with Pipeline(p, 34, 30) as b:
+        b.restore(snap)
+        rest_b = [b.process_frame(f) for f in frames[7:]]
+    for x, y in zip(rest_a, rest_b):
+        assert np.array_equal(x.residual, y.residual)
+        assert np.array_equal(x.velocity.indices, y.velocity.indices)
