@@ -14,6 +14,11 @@ The per-pixel state (1.6 KB/px, 0.5 GB per stream) is larger than L2, so
 no L2 flush is needed between steps.  Under torchrun (N > 1) every rank runs
 an independent 640x512 sensor stream on its own GPU (streams
 shard with no exchange), timed between barriers, max over ranks.
+``--gpus N`` without torchrun re-launches this script under
+torch.distributed.run with N processes.  The same JSON line carries, under
+``c4_strip_sharded``, config C4: one 4096x4096 frame stream split into N
+row strips (strips.py), the per-frame NCCL halo exchange inside the timed
+region (strong scaling: the total work is fixed).
 
 ``--impl reference`` times the reference algorithm on the host cores: the
 float64 C restatement in oracle/ (bit-exact to the reference package, see
@@ -38,6 +43,9 @@ sys.path.insert(0, ROOT)
 
 WIDTH, HEIGHT = 640, 512
 METRIC = "pixel-frames/sec (640x512, full pipeline)"
+WORKLOAD = "C3: 640x512 frames, full SDFT->deadbeat->autocorr->PEF chain, default FilterParams"
+DATA = ("synthetic (reference scene model: 25 drifting cosines + target + counter-based noise, "
+        "scenegen.generate_device / generate_counter, seed = rank)")
 UNIT = "px-frames/s"
 FALLBACK_HBM_GBS = 6650.0
 
@@ -159,46 +167,46 @@ def cpu_oracle_rate(params, frames_np, budget_s=12.0, threads=None, max_frames=6
 
 
 def run_reference(args):
-    """--impl reference: the reference algorithm (float64 oracle, bit-exact to
-    the reference package) on all host cores, same config/metric."""
+    """--impl reference: the reference algorithm (the float64 C oracle,
+    bit-exact to the reference package) on all host cores, on the GPU arm's
+    workload -- the same full 640x512 frames (generate_counter, seed 0, bit
+    for bit the frames the GPU arm's rank 0 generates on the device), same
+    metric.  Each step is one whole frame; the number of timed steps is
+    capped so that the run ends within a few minutes."""
     world, rank, _ = dist_setup()
     if rank != 0:
         return
     from paper_1408_3526_b200 import default_params
-    from paper_1408_3526_b200.scenegen import SimConfig, generate
+    from paper_1408_3526_b200.scenegen import SimConfig, generate_counter
     from oracle.oracle import OraclePipeline
 
     p = default_params()
     threads = os.cpu_count() or 1
-    # bounded sample: size the crop height so the whole run fits ~150 s
-    probe_h = 64
-    frames, _ = generate(SimConfig(width=WIDTH, height=probe_h, frame_count=8, rng_seed=0))
-    with OraclePipeline(p, WIDTH, probe_h, threads=threads) as orc:
-        for f in frames[:6]:
-            orc.process_frame(f)
-        t0 = time.perf_counter()
-        orc.process_frame(frames[6])
-        per_row = (time.perf_counter() - t0) / probe_h
-    total = args.steps + args.warmup + p.mz
-    rows = int(min(HEIGHT, max(16, 150.0 / max(total, 1) / max(per_row, 1e-9))))
-    n_frames = min(total, 64)
-    frames, _ = generate(SimConfig(width=WIDTH, height=rows, frame_count=max(n_frames, 5), rng_seed=0))
-    with OraclePipeline(p, WIDTH, rows, threads=threads) as orc:
-        for k in range(p.mz - 1 + args.warmup):
-            orc.process_frame(frames[k % len(frames)])
-        t0 = time.perf_counter()
-        for k in range(args.steps):
-            orc.process_frame(frames[(p.mz - 1 + args.warmup + k) % len(frames)])
-        dt = time.perf_counter() - t0
-    value = args.steps * rows * WIDTH / dt
-    sample = (f"{args.steps} steady-state frames of a 640x{rows} crop of the C3 scene "
-              f"(float64 C oracle = reference algorithm, {threads} threads)")
+    cfg = SimConfig(width=WIDTH, height=HEIGHT, frame_count=1000, rng_seed=0)
+    n_frames = 24  # generated once, cycled (the state never repeats: it is recursive)
+    frames = generate_counter(cfg, frames=n_frames)
+    with OraclePipeline(p, WIDTH, HEIGHT, threads=threads) as orc:
+        k = 0
+        for _ in range(p.mz - 1 + args.warmup):
+            orc.process_frame(frames[k % n_frames])
+            k += 1
+        budget_s = args.ref_budget
+        done, dt = 0, 0.0
+        while done < args.steps and (dt < budget_s or done < 3):
+            t0 = time.perf_counter()
+            orc.process_frame(frames[k % n_frames])
+            dt += time.perf_counter() - t0
+            k += 1
+            done += 1
+    value = done * HEIGHT * WIDTH / dt
+    sample = (f"{done} steady-state 640x512 frames of the C3 scene (of {args.steps} requested; capped at "
+              f"{budget_s:.0f} s of CPU time), float64 C oracle = reference algorithm, {threads} threads")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
+        "steps": done, "steps_requested": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / done,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (reference scene generator)",
-        "config": {"workload": f"C3 640x{rows} crop, full pipeline, default FilterParams", "frame": [WIDTH, rows]},
+        "data": DATA,
+        "config": {"workload": WORKLOAD, "frame": [WIDTH, HEIGHT], "streams": 1},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
@@ -220,6 +228,9 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
 
+        # NCCL's communicator-init log (ranks, transports) for the record
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     p = default_params()
@@ -292,24 +303,34 @@ def run_ours(args):
             yield host_np[(start + i) % n_host]
 
     with PublicPipeline(p, WIDTH, HEIGHT, device=local) as pub:
-        for _ in pub.process_stream(host_frames(0, p.mz - 1 + args.warmup)):
-            pass
+        # one stream, timed in steady state: the first outputs (temporal
+        # window + warm-up, pipeline filling) are consumed before the clock
+        # starts; every timed step still uploads its frame and downloads its
+        # outputs inside the timed region
+        n_pre = p.mz - 1 + args.warmup
+        stream_it = pub.process_stream(host_frames(0, n_pre + e2e_steps))
+        for _ in range(args.warmup):
+            next(stream_it)
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         n_out = 0
-        for out in pub.process_stream(host_frames(p.mz - 1 + args.warmup, e2e_steps)):
+        for out in stream_it:
             n_out += 1
         e2e_s = time.perf_counter() - t0
-        # the synchronous reference-style call, for the record
-        t0 = time.perf_counter()
+        # the synchronous reference-style call, for the record (warmed up)
         sync_steps = min(e2e_steps, 200)
+        for i in range(args.warmup):
+            pub.process_frame(host_np[i % n_host])
+        t0 = time.perf_counter()
         for i in range(sync_steps):
             out_sync = pub.process_frame(host_np[i % n_host])
         sync_s = time.perf_counter() - t0
         # ... and with ordinary (pageable) numpy frames, as a reference user passes them
         page_np = host_np[: min(n_host, 16)].copy()
+        for i in range(args.warmup):
+            pub.process_frame(page_np[i % page_np.shape[0]])
         t0 = time.perf_counter()
         for i in range(sync_steps):
             out_sync = pub.process_frame(page_np[i % page_np.shape[0]])
@@ -349,15 +370,14 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (reference scene model: 25 drifting cosines + target + noise, generated on device)",
-            "config": {"workload": "C3: 640x512 frames, full SDFT->deadbeat->autocorr->PEF chain, default FilterParams",
-                       "frame": [WIDTH, HEIGHT], "streams": world,
+            "data": DATA,
+            "config": {"workload": WORKLOAD, "frame": [WIDTH, HEIGHT], "streams": world,
                        "parallelism": "independent stream per GPU" if world > 1 else "single GPU",
                        "l2": "state 0.5 GB/stream >> 126 MB L2 (no flush needed)",
                        "grid": info["grid"], "block": info["block"], "smem_bytes": info["smem_bytes"]},
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "api": "Pipeline.process_stream (pinned host frames in; host residual, prediction, "
-                           "velocity pairs out per step; depth-3 pipelining)",
+                           "velocity pairs out per step; depth-3 pipelining, timed in steady state)",
                     "sync_process_frame": {"value": e2e_sync, "unit": UNIT, "steps": sync_steps,
                                            "frames": "pinned"},
                     "sync_process_frame_pageable": {"value": e2e_sync_page, "unit": UNIT, "steps": sync_steps,
@@ -367,9 +387,59 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),
         }
+    c4 = None if args.no_c4 else c4_strip_line(args, lib, dist, world, rank, local, dev)
+    if rank == 0:
+        line["c4_strip_sharded"] = c4
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def c4_strip_line(args, lib, dist, world, rank, local, dev):
+    """Config C4 (BASELINE.json): one 4096x4096 stream split into `world`
+    row strips (strips.py); each timed step = this rank's NCCL halo
+    exchange (My-1 rows from the rank above) + assembly + the fused kernel
+    on its strip.  Device time on a dedicated stream, barriers on both sides,
+    max over ranks; value = 4096^2 px per step over that time."""
+    import torch
+
+    from paper_1408_3526_b200 import default_params
+    from paper_1408_3526_b200.scenegen import SimConfig, generate_device
+    from paper_1408_3526_b200.strips import StripPipeline
+
+    w = h = 4096
+    p = default_params()
+    steps = min(args.steps, args.c4_steps)
+    stream = torch.cuda.Stream(device=dev)
+    prev = torch.cuda.current_stream(dev)
+    torch.cuda.set_stream(stream)
+    sp = StripPipeline(p, w, h, rank, world, device=local)
+    pl = sp.plan
+    own = generate_device(SimConfig(width=w, height=h, frame_count=200, rng_seed=4), device=dev, frames=6,
+                          rows=(pl.a0, pl.a1))
+    el, kern, n, clk = _device_run(lib, sp.pipe, own, steps, args.warmup, stream, dist, before_push=sp.assemble)
+    sp.close()
+    del own
+    torch.cuda.set_stream(prev)
+    t = torch.tensor([el, kern], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    el, kern = float(t[0]), float(t[1])
+    peak, peak_kind = measured_peak()
+    bpp = b_alg(p)
+    rows = pl.a1 - pl.a0  # anchor rows of the largest strip (ranks are equal to +-1 row)
+    achieved = bpp * rows * w / (kern / 1e3) / 1e9
+    return {
+        "metric": "pixel-frames/sec (4096x4096, strip-sharded)", "value": w * h * steps / (el / 1e3), "unit": UNIT,
+        "n_gpus": world, "steps": steps, "ms_per_step": el / steps, "scaling": "strong",
+        "config": {"workload": "C4: 4096x4096 frames, row strips + (My-1)-row halo exchanged per frame over "
+                               + ("NCCL" if dist else "nothing (one strip)"),
+                   "frame": [w, h], "strips": world, "strip_rows": rows, "halo_rows": pl.halo},
+        "gpu_launches": steps, "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                                            "frac": achieved / peak, "peak_kind": peak_kind, "kernel_ms": kern,
+                                            "bytes_per_px_frame": bpp},
+        "clocks": clk,
+    }
 
 
 # ---------------------------------------------------------------------------
@@ -582,6 +652,22 @@ def run_config(args):
         dist.destroy_process_group()
 
 
+def relaunch(n: int) -> int:
+    """`--gpus N` outside torchrun: run this script again as N ranks, one per
+    GPU (torch.distributed.run, 127.0.0.1), NCCL's init log enabled."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd, env=env).returncode
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
@@ -590,11 +676,17 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU-oracle timing")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c4", action="store_true", help="skip the C4 strip-sharded block of the headline line")
+    ap.add_argument("--c4-steps", type=int, default=400, help="timed frames of the C4 block (capped by --steps)")
+    ap.add_argument("--ref-budget", type=float, default=60.0,
+                    help="--impl reference: seconds of timed CPU work (steps are capped to fit)")
     ap.add_argument("--config", choices=("c3", "c2", "c4", "c4strips", "c5", "c3naive", "c3seq"), default="c3",
                     help="c3 (default, the headline) or another BASELINE.json configuration")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args.gpus))
     if args.impl == "reference":
         run_reference(args)
     elif args.config != "c3":

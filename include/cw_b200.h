@@ -113,6 +113,18 @@ int cw_submit(cw_handle *h, const float *frame, float *residual, float *predicti
 int cw_wait(cw_handle *h, int64_t ticket, int32_t *ready, int64_t *frame_index);
 
 /*
+ * cw_submit for a frame already in device memory (a strip assembled from
+ * NCCL halo receives, strips.py): the pipeline's stream waits for work
+ * already enqueued on `producer` (a cudaStream_t; NULL = legacy default),
+ * copies the frame into its ring slot, and `producer` is then ordered after
+ * that copy, so the caller may refill `frame_dev` with work enqueued later
+ * on `producer`.  Results download into the host buffers as cw_submit's;
+ * collect them with cw_wait(ticket).
+ */
+int cw_submit_device(cw_handle *h, const float *frame_dev, float *residual, float *prediction, uint8_t *vidx,
+                     int64_t *ticket, void *producer);
+
+/*
  * cw_submit for a frame in a sequence-file sample format (replaces the host
  * decode of read_sequence, seqio.py:172-204; the payloads of seqio.py:1-8):
  *   CW_FMT_F32LE: little-endian float32 (frames.f32), scale/offset ignored;

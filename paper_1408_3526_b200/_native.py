@@ -36,6 +36,7 @@ EXPORTS = (
     "cw_kernel_time", "cw_copy_to_host", "cw_submit", "cw_submit_raw", "cw_wait", "cw_set_detection", "cw_detections",
     "cw_set_backend", "cw_snapshot_size", "cw_snapshot", "cw_restore",
     "cw_scene_generate", "cw_scene_last_error", "cw_index_bytes", "cw_is_generic",
+    "cw_submit_device",
 )
 
 
@@ -162,6 +163,7 @@ def load():
         "cw_submit": (ctypes.c_int, [vp, vp, vp, vp, vp, P(i64)]),
         "cw_submit_raw": (ctypes.c_int, [vp, vp, i32, ctypes.c_double, ctypes.c_double, vp, vp, vp, P(i64)]),
         "cw_wait": (ctypes.c_int, [vp, i64, P(i32), P(i64)]),
+        "cw_submit_device": (ctypes.c_int, [vp, vp, vp, vp, vp, P(i64), vp]),
         "cw_set_detection": (ctypes.c_int, [vp, ctypes.c_float, i32]),
         "cw_set_backend": (ctypes.c_int, [vp, i32]),
         "cw_snapshot_size": (ctypes.c_int, [vp, P(ctypes.c_size_t)]),

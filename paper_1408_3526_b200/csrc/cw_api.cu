@@ -1150,6 +1150,58 @@ static int submit_impl(cw_handle *h, const void *samples, int format, double sca
     return CW_OK;
 }
 
+// Pipelined push of a frame already in device memory (e.g. a strip
+// assembled from NCCL halo receives): the handle's stream waits for the
+// producer stream, copies the frame into its ring slot, and the producer
+// stream is then ordered after that copy (the caller may overwrite its
+// buffer with work enqueued later on `producer`); kernel and result download
+// overlap the next frames exactly as cw_submit's.
+int cw_submit_device(cw_handle *h, const float *frame_dev, float *residual, float *prediction, uint8_t *vidx,
+                     int64_t *ticket, void *producer)
+{
+    NvtxRange nvtx("cw_submit_device");
+    DeviceGuard dg(h);
+    if (!h || !frame_dev || !ticket)
+        return CW_ERR_VALUE;
+    const size_t HW = (size_t)h->W * h->H;
+    const long long n = h->frames_seen;
+    const int e = (int)(n % cw_handle::NEV);
+    if (n >= cw_handle::NEV)  // ticket n - NEV must have been collected
+        CW_CUDA(h, cudaEventSynchronize(h->ev_down[e]));
+    cudaStream_t ps = reinterpret_cast<cudaStream_t>(producer);
+    CW_CUDA(h, cudaEventRecord(h->ev_up[e], ps));
+    CW_CUDA(h, cudaStreamWaitEvent(h->own, h->ev_up[e], 0));
+    float *slot = h->d_frames + (size_t)(n % h->nslots) * HW;
+    if (slot != frame_dev)
+        CW_CUDA(h, cudaMemcpyAsync(slot, frame_dev, HW * 4, cudaMemcpyDeviceToDevice, h->own));
+    CW_CUDA(h, cudaEventRecord(h->ev_up[e], h->own));
+    CW_CUDA(h, cudaStreamWaitEvent(ps, h->ev_up[e], 0));
+    if (n >= 2)
+        CW_CUDA(h, cudaStreamWaitEvent(h->own, h->ev_down[(n - 2) % cw_handle::NEV], 0));
+    int32_t rd = 0;
+    int64_t fi = -1;
+    const size_t set = (size_t)(n & 1);
+    int rc = run_frame(h, h->own, &rd, &fi);
+    if (rc != CW_OK)
+        return rc;
+    CW_CUDA(h, cudaEventRecord(h->ev_k[e], h->own));
+    CW_CUDA(h, cudaStreamWaitEvent(h->down, h->ev_k[e], 0));
+    const size_t vb = HW * 2 * h->idx_bytes;
+    if (rd) {
+        if (residual)
+            CW_CUDA(h, cudaMemcpyAsync(residual, h->d_res + set * HW, HW * 4, cudaMemcpyDeviceToHost, h->down));
+        if (prediction)
+            CW_CUDA(h, cudaMemcpyAsync(prediction, h->d_pred + set * HW, HW * 4, cudaMemcpyDeviceToHost, h->down));
+        if (vidx)
+            CW_CUDA(h, cudaMemcpyAsync(vidx, h->d_vidx + set * vb, vb, cudaMemcpyDeviceToHost, h->down));
+    }
+    CW_CUDA(h, cudaEventRecord(h->ev_down[e], h->down));
+    h->ready_of[e] = rd;
+    h->fidx_of[e] = fi;
+    *ticket = n;
+    return CW_OK;
+}
+
 int cw_wait(cw_handle *h, int64_t ticket, int32_t *ready, int64_t *frame_index)
 {
     DeviceGuard dg(h);

@@ -83,15 +83,24 @@ def exchange_halo(own_rows, plan: StripPlan, halo: int, group=None):
     import torch
     import torch.distributed as dist
 
+    if plan.world == 1:
+        return None  # one strip: nothing crosses
+    # gloo moves host tensors only: stage CUDA rows through the host there
+    staged = own_rows.is_cuda and dist.get_backend(group) == "gloo"
+    dev = own_rows.device
     ops, recv = [], None
     if plan.halo:
-        recv = torch.empty((plan.halo, own_rows.shape[1]), dtype=own_rows.dtype, device=own_rows.device)
+        recv = torch.empty((plan.halo, own_rows.shape[1]), dtype=own_rows.dtype,
+                           device="cpu" if staged else dev)
         ops.append(dist.P2POp(dist.irecv, recv, plan.rank - 1, group=group))
     if plan.rank + 1 < plan.world:
-        ops.append(dist.P2POp(dist.isend, own_rows[-halo:].contiguous(), plan.rank + 1, group=group))
+        send = own_rows[-halo:].contiguous()
+        ops.append(dist.P2POp(dist.isend, send.cpu() if staged else send, plan.rank + 1, group=group))
     if ops:
         for req in dist.batch_isend_irecv(ops):
             req.wait()
+    if staged and recv is not None:
+        recv = recv.to(dev)
     return recv
 
 
@@ -119,18 +128,71 @@ class StripPipeline:
         self.device = torch.device("cuda", device)
         self.pipe = Pipeline(params, width, self.plan.local_height, device=device, bank=bank,
                              _strip=(self.plan.halo, self.plan.lo))
-        self._frame = torch.empty((self.plan.local_height, width), dtype=torch.float32, device=self.device)
+        # two assembly buffers: frame n+1 is assembled while frame n's copy
+        # into the pipeline's ring slot may still be queued
+        self._frames = [torch.empty((self.plan.local_height, width), dtype=torch.float32, device=self.device)
+                        for _ in range(2)]
+        self._k = 0
 
     def assemble(self, own_rows):
-        """Local strip frame = [halo rows from rank-1 ; own rows]."""
+        """Local strip frame = [halo rows from rank-1 ; own rows], on torch's
+        current stream."""
+        frame = self._frames[self._k & 1]
+        self._k += 1
         halo = exchange_halo(own_rows, self.plan, self.halo, self.group)
         if halo is not None:
-            self._frame[: self.plan.halo].copy_(halo)
-        self._frame[self.plan.halo:].copy_(own_rows)
-        return self._frame
+            frame[: self.plan.halo].copy_(halo)
+        frame[self.plan.halo:].copy_(own_rows)
+        return frame
 
     def process_frame(self, own_rows):
         return self.pipe.process_frame_device(self.assemble(own_rows))
+
+    def process_stream(self, rows, depth: int = 3):
+        """Pipelined ``process_frame`` over an iterable of this rank's
+        (a1 - a0, W) CUDA row blocks: the halo exchange and assembly of frame
+        n+1, the fused kernel of frame n and the download of frame n-1 into
+        pinned host buffers overlap (cw_submit_device / cw_wait).  Yields the
+        local WhitenedOutput of every ready frame, in order."""
+        import ctypes
+        from collections import deque
+
+        import torch
+
+        from . import _native
+
+        lib = _native.load()
+        pipe = self.pipe
+        h, w = self.plan.local_height, self.width
+        inflight: deque = deque()
+
+        def collect():
+            ticket, res, pred, vidx = inflight.popleft()
+            ready, fidx = ctypes.c_int32(0), ctypes.c_int64(-1)
+            _native.check(lib.cw_wait(pipe._h, ticket, ctypes.byref(ready), ctypes.byref(fidx)), pipe._h)
+            return pipe._wrap(int(fidx.value), res, pred, vidx, ticket=ticket) if ready.value else None
+
+        try:
+            for own in rows:
+                frame = self.assemble(own)
+                res, pred, vidx = pipe._pool.take_outputs(h, w, pipe._idx_bytes)
+                ticket = ctypes.c_int64(-1)
+                stream = torch.cuda.current_stream(self.device)
+                _native.check(lib.cw_submit_device(pipe._h, ctypes.c_void_p(frame.data_ptr()), res.ctypes.data,
+                                                   pred.ctypes.data, vidx.ctypes.data, ctypes.byref(ticket),
+                                                   ctypes.c_void_p(stream.cuda_stream)), pipe._h)
+                inflight.append((ticket.value, res, pred, vidx))
+                while len(inflight) > depth:
+                    out = collect()
+                    if out is not None:
+                        yield out
+            while inflight:
+                out = collect()
+                if out is not None:
+                    yield out
+        finally:
+            while inflight:
+                lib.cw_wait(pipe._h, inflight.popleft()[0], None, None)
 
     def output_rows(self):
         """(global first residual row, local slice) and (global first
