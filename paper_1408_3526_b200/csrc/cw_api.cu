@@ -97,6 +97,10 @@ struct cw_handle {
     void *d_gtab = nullptr;
     float2 *d_xf = nullptr;
     int nxf = 0;  // x-stage frames allocated
+    // fused kernel work split (FrameArgs.work): static fraction + dynamic chunks
+    unsigned int *d_work = nullptr;
+    double dyn_static = 0.92;  // measured on C3 (tools/ab_kernel.py): 0.92 / 2 rows, ~1% faster than all-static
+    int dyn_chunk = 2;
     int nslots = 0;  // frame ring slots: max(mhat_z + 2, Mz + 1) (async upload spare; naive window)
     bool naive = false;  // spectrum backend: false = recursive (observer), true = naive window DFT
     int naive_grid = 0;
@@ -465,12 +469,26 @@ static int build_coef(cw_handle *h, const float *bank, const int64_t *retained, 
         };
         float *o = out->data() + (size_t)v * NRET;
         int w = 0;
+        // pred += p.x z.r + p.y z.i = Re(k z), k = (p.x, -p.y); a kernel that
+        // reads the stored (rotated) state z = w z+ instead of z+ gets
+        // k conj(w(kz)) (fold_w)
+        const double PI = 3.14159265358979323846;
+        auto put = [&](int kz, double px, double py) {
+            if (h->fn.pef_l2 && kz != 0) {
+                const double wr = std::cos(2 * PI * kz / Mz), wi = std::sin(2 * PI * kz / Mz);
+                const double kr = px, ki = -py;  // k conj(w)
+                const double nr = kr * wr + ki * wi, ni = ki * wr - kr * wi;
+                px = nr;
+                py = -ni;
+            }
+            o[w++] = (float)px;
+            o[w++] = (float)py;
+        };
         auto pair = [&](int kz, int ky, int kx) -> bool {
             double cr, ci, dr, di;
             if (!coef(kz, ky, kx, &cr, &ci) || !coef(-kz, -ky, -kx, &dr, &di))
                 return false;
-            o[w++] = (float)(cS * (cr + dr));
-            o[w++] = (float)(cS * (di - ci));
+            put(kz, cS * (cr + dr), cS * (di - ci));
             return true;
         };
         // row 0: DC bin (kz = 0 real, kz = 1..KZ), then kx = 1..BX, all kz
@@ -641,6 +659,13 @@ int cw_create(const cw_params *p, int32_t width, int32_t height, int32_t device,
             return cleanup_fail(CW_ERR_CUDA, "cudaEventCreate failed");
     if (!generic)
         cudaMemcpyAsync(h->d_coef, coef.data(), coef.size() * 4, cudaMemcpyHostToDevice, h->own);
+    if (const char *e = std::getenv("CW_DYN_STATIC"))  // tuning knobs (tools/ab_kernel.py)
+        h->dyn_static = std::atof(e);
+    if (const char *e = std::getenv("CW_DYN_CHUNK"))
+        h->dyn_chunk = std::max(1, std::atoi(e));
+    if (cudaMalloc(&h->d_work, 2 * sizeof(unsigned int)) != cudaSuccess)
+        return cleanup_fail(CW_ERR_NOMEM, "device allocation failed");
+    cudaMemsetAsync(h->d_work, 0, 2 * sizeof(unsigned int), h->own);
     if (cudaStreamSynchronize(h->own) != cudaSuccess)
         return cleanup_fail(CW_ERR_CUDA, "device initialisation failed");
     *out = h;
@@ -663,6 +688,7 @@ void cw_destroy(cw_handle *h)
     cudaFree(h->d_pred);
     cudaFree(h->d_vidx);
     cudaFree(h->d_gtab);
+    cudaFree(h->d_work);
     cudaFree(h->d_xf);
     cudaFree(h->d_det);
     if (h->h_det)
@@ -765,6 +791,16 @@ static int run_frame(cw_handle *h, cudaStream_t s, int32_t *ready, int64_t *fram
     a.forced_iy = h->forced_iy;
     a.mhx = h->mhx;
     a.mhy = h->mhy;
+    {
+        const long long units = (long long)h->NXB * (h->H - h->halo);
+        const long long su = (long long)(h->dyn_static * (double)units);
+        // dynamic chunks pay a run restart each: only for long per-CTA runs
+        const bool dyn = h->dyn_static < 1.0 && su < units && units >= 20LL * h->grid;
+        a.work = dyn ? h->d_work : nullptr;
+        a.parity = (int)(n & 1);
+        a.static_units = su < 0 ? 0 : su;
+        a.dyn_chunk = h->dyn_chunk;
+    }
     a.det = nullptr;
     a.det_tau = h->det_tau;
     a.det_cap = h->det_cap;

@@ -60,6 +60,12 @@ constexpr int RESTART = CW_RESTART;  // rows between direct y-SDFT restarts (bou
 #ifndef CW_TMA_CHUNKS
 #define CW_TMA_CHUNKS 1  // bulk copies per state packet (1: one copy per row, measured fastest)
 #endif
+#ifndef CW_PEF_L2
+// PEF reads the retained z+ back from the state row just written to HBM
+// (an L2 hit; z+ = conj(w) z, conj(w) folded into the coefficients on the
+// host) instead of a 32 KB retained-z+ stage in shared memory
+#define CW_PEF_L2 0
+#endif
 #ifndef CW_FENCE_ALL
 #define CW_FENCE_ALL 1  // every thread orders its generic stage reads before the next TMA write
 #endif
@@ -118,6 +124,15 @@ struct FrameArgs {
     int y_off;             // global row of local row 0
     int ready, first;      // flow/PEF enabled; first ready frame (T^ := T)
     int forced_ix, forced_iy;  // < 0: no override
+    // work split: the first static_units (column-block, row) units are dealt
+    // out in equal contiguous runs, the rest in dyn_chunk-row chunks that
+    // CTAs claim from work[parity] (atomic counter; the kernel zeroes
+    // work[parity ^ 1] for the next launch): CTAs that run slower (die,
+    // L2-slice distance, SM-mate) take fewer chunks, so they all end together
+    unsigned int *work;
+    int parity;
+    long long static_units;
+    int dyn_chunk;
     int mhx, mhy;
     // detection epilogue (nullable): 64-byte header {u32 count; u64 peak
     // key; -; u64 n valid}, f64 sum res^2 per (local row, column block)
@@ -194,7 +209,7 @@ struct Geo {
     // shared memory plan (bytes)
     static constexpr int SM_STAGE = NSP * 32 * 8;     // state packet -> Cx in place
     static constexpr int SM_TSTAGE = NTP * 32 * 8;    // T^ packet
-    static constexpr int SM_RET = RETPP * 32 * 8;     // retained z+ quads
+    static constexpr int SM_RET = CW_PEF_L2 ? 0 : RETPP * 32 * 8;  // retained z+ quads
     static constexpr int SM_XF = RING * XF * 32 * 4;  // x-stage ring
     static constexpr int SM_BEST = NR * 32 * 8;       // partial argmax (score, rank)
     static constexpr int SM_PEF = (BY + 1) * 32 * 4;
@@ -324,6 +339,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase)
 #ifdef CW_PHASE_TIMING
 // per-warp clock64 accumulators (phase-timing builds only): [warp][event]
 __device__ unsigned long long cw_phase_clk[8][16];
+// per-CTA %globaltimer (ns) at kernel entry and exit, last launch: [cta][2]
+__device__ unsigned long long cw_cta_span[1024][2];
+__device__ __forceinline__ unsigned long long cw_gtimer()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
+    return t;
+}
 // the "memory" clobber pins each stamp between the surrounding barriers and
 // shared-memory accesses (a plain clock64() may be moved across them)
 __device__ __forceinline__ unsigned long long cw_clock_pinned()
@@ -372,6 +395,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
 #ifdef CW_PHASE_TIMING
     unsigned long long clk_prev = cw_clock_pinned();
     unsigned long long clk_acc[11] = {};
+    if (threadIdx.x == 0 && blockIdx.x < 1024) cw_cta_span[blockIdx.x][0] = cw_gtimer();
 #endif
     constexpr int KX = G::KX, KY = G::KY, KZ = G::KZ, BX = G::BX, BY = G::BY;
     constexpr int MX = G::MX, MY = G::MY, MZ = G::MZ;
@@ -395,8 +419,10 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
     const int nlx = NL ? NL : t.nlx, nly = NL ? NL : t.nly;
     const int rows = H - a.y_begin;
     const long long units = (long long)NXB * rows;
-    const long long u0 = units * blockIdx.x / gridDim.x;
-    const long long u1 = units * (blockIdx.x + 1) / gridDim.x;
+    const long long su = a.work ? a.static_units : units;
+    long long u = su * blockIdx.x / gridDim.x;
+    long long u1 = su * (blockIdx.x + 1) / gridDim.x;
+    __shared__ long long s_claim;
     const bool use_that = a.ready && !a.first;
 
     uint8_t *srxy = reinterpret_cast<uint8_t *>(srank + MAXL * MAXL);  // rank -> (ix, iy)
@@ -412,6 +438,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
         mbar_init(bar_t, 1);
         fence_mbar_init();
     }
+    if (a.work && blockIdx.x == 0 && threadIdx.x == 0) a.work[a.parity ^ 1] = 0u;
     __syncthreads();
     uint32_t phase = 0, phase_t = 0;
 
@@ -504,8 +531,18 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
         return c2(stage[(G::spair(rr) + (kx + KX) * MZ + (kz + KZ)) * 32 + lane]);
     };
 
-    long long u = u0;
-    while (u < u1) {
+    for (;;) {
+        if (u >= u1) {  // static run done: claim the next dynamic chunk
+            if (!a.work) break;
+            if (threadIdx.x == 0) {
+                const unsigned int k = atomicAdd(a.work + a.parity, 1u);
+                s_claim = su + (long long)k * a.dyn_chunk;
+            }
+            __syncthreads();
+            u = s_claim;
+            if (u >= units) break;
+            u1 = u + a.dyn_chunk < units ? u + a.dyn_chunk : units;
+        }
         const int xb = (int)(u / rows);
         const int ys = a.y_begin + (int)(u % rows);
         const long long left = u1 - u;
@@ -561,7 +598,9 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
             // z+ is exactly the reference's unnormalised temporal DFT of the
             // last Mz spatial spectra (_kernels.py:71-90, S = norm * z+).
             // retained z+ (the PEF input), pair q of the padded layout
-            auto rput = [&](int q, cf v) { sret[q * 32 + lane] = f2(v); };
+            auto rput = [&](int q, cf v) {
+                if (!CW_PEF_L2) sret[q * 32 + lane] = f2(v);
+            };
             cf cz[MX][MZ];  // 4 x Hz(z+) per kx column
             if (CW_MEMONLY) {  // diagnostic: the same HBM traffic, no arithmetic
                 const int np = r == 0 ? G::ROW0P : G::ROWNP;
@@ -1045,7 +1084,13 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                 // (one 16-byte coefficient load, one retained quad) per step
                 const float4 *cp = reinterpret_cast<const float4 *>(a.coefP + (size_t)(viy * nlx + vix) * G::RETPP) +
                                    G::pquad(r);
-                const float2 *sr = sret + 2 * G::pquad(r) * 32 + lane;
+                // retained pair q of row r: smem stage, or the state row in
+                // L2 (row 0: pair q; rows >= 1: pair q + (KX - BX) MZ; the odd
+                // pad pair has a zero coefficient and reads a real pair)
+                const float2 *sr = CW_PEF_L2
+                    ? a.state + ((CW_L2ONLY ? (size_t)blockIdx.x : (size_t)yy * NXB + xb) * G::NSP + G::spair(r) +
+                                 (r == 0 ? 0 : (KX - BX) * MZ)) * 32 + lane
+                    : sret + 2 * G::pquad(r) * 32 + lane;
                 cf acc[2] = {cmk(0.f, 0.f), cmk(0.f, 0.f)};  // packed (c.x z.x, c.y z.y) partial sums
                 auto quad = [&](int k) {
                     const float4 c = ldg_coef4(cp + k);
@@ -1094,6 +1139,8 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
 #ifdef CW_PHASE_TIMING
     if (blockIdx.x == 0 && (threadIdx.x & 31) == 0)
         for (int k = 0; k < 11; k++) cw_phase_clk[threadIdx.x >> 5][k] += clk_acc[k];
+    __syncthreads();
+    if (threadIdx.x == 0 && blockIdx.x < 1024) cw_cta_span[blockIdx.x][1] = cw_gtimer();
 #endif
 #undef XFR
 }

@@ -16,14 +16,16 @@ struct LaunchFn {
     size_t smem;
     int nsp, ntp, retp;  // float2 pairs per pixel: observer state, T^, retained (PEF rows padded)
     int nl;              // compiled lag count (0: runtime loops)
+    int pef_l2;          // CW_PEF_L2 build: PEF coefficients carry conj(w(kz))
     void (*phase_clocks)(unsigned long long *dst);  // CW_PHASE_TIMING builds: this unit's clocks
 };
 
 #ifdef CW_PHASE_TIMING
-static void phase_clocks_read(unsigned long long *dst)  // [8][16], then zeroed
+static void phase_clocks_read(unsigned long long *dst)  // [8][16] + CTA spans [1024][2], clocks zeroed
 {
     cudaDeviceSynchronize();
     cudaMemcpyFromSymbol(dst, cw_phase_clk, sizeof(unsigned long long) * 128);
+    cudaMemcpyFromSymbol(dst + 128, cw_cta_span, sizeof(unsigned long long) * 2048);
     static unsigned long long zero[128] = {};
     cudaMemcpyToSymbol(cw_phase_clk, zero, sizeof zero);
 }
@@ -81,6 +83,7 @@ LaunchFn make_inst()
     f.ntp = G::NTP;
     f.retp = G::RETPP;
     f.nl = NL;
+    f.pef_l2 = CW_PEF_L2;
 #ifdef CW_PHASE_TIMING
     f.phase_clocks = &phase_clocks_read;
 #endif
