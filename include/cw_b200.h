@@ -185,6 +185,17 @@ int32_t cw_index_bytes(const cw_handle *h);
  * params.py:114-158 accepts), 0 for the fused kernel. */
 int32_t cw_is_generic(const cw_handle *h);
 
+/* Which kernel runs this handle: 0 = a fused instance compiled into the
+ * library, 1 = a fused instance compiled at run time for this geometry
+ * (NVRTC, cached as a cubin), 2 = the runtime-geometry kernels. */
+int32_t cw_kernel_kind(const cw_handle *h);
+
+/* Compile (NVRTC) the fused instance these parameters need into the cubin
+ * cache directory `dir` unless it is there already (build-time prebuild;
+ * the library looks in <package>/jit_cache).  CW_ERR_UNSUPPORTED when the
+ * geometry is beyond the fused kernel or NVRTC is unavailable. */
+int cw_jit_prebuild(const cw_params *params, const char *dir);
+
 /* Spectrum backend (pipeline.py:139-142): 0 = recursive (sliding DFT +
  * deadbeat observer, default), 1 = naive: every pixel's spectrum evaluated
  * directly from its raw Mx x My x Mz window (spectrum.py:257-327), then the

@@ -36,7 +36,7 @@ EXPORTS = (
     "cw_kernel_time", "cw_copy_to_host", "cw_submit", "cw_submit_raw", "cw_wait", "cw_set_detection", "cw_detections",
     "cw_set_backend", "cw_snapshot_size", "cw_snapshot", "cw_restore",
     "cw_scene_generate", "cw_scene_last_error", "cw_index_bytes", "cw_is_generic",
-    "cw_submit_device",
+    "cw_submit_device", "cw_kernel_kind", "cw_jit_prebuild",
 )
 
 
@@ -78,7 +78,8 @@ def build(verbose: bool = False, out: str | None = None, dev: bool = False, extr
     with tempfile.TemporaryDirectory(prefix="cw_build_") as tmp:
         omp = ["-Xcompiler", "-fopenmp"] if openmp else []
         jobs = [["nvcc", *base, *omp, "-c", "-o", os.path.join(tmp, "cw_api.o"), os.path.join(CSRC, "cw_api.cu")],
-                ["nvcc", *base, "-c", "-o", os.path.join(tmp, "cw_generic.o"), os.path.join(CSRC, "cw_generic.cu")]]
+                ["nvcc", *base, "-c", "-o", os.path.join(tmp, "cw_generic.o"), os.path.join(CSRC, "cw_generic.cu")],
+                ["nvcc", *base, "-c", "-o", os.path.join(tmp, "cw_jit.o"), os.path.join(CSRC, "cw_jit.cu")]]
         for inst in instances(dev):
             defs = [f"-DCW_{k}={v}" for k, v in zip(("IKX", "IKY", "IKZ", "IBX", "IBY", "INL"), inst)]
             obj = os.path.join(tmp, "cw_inst_" + "_".join(map(str, inst)) + ".o")
@@ -99,6 +100,39 @@ def build(verbose: bool = False, out: str | None = None, dev: bool = False, extr
                         *(["-lgomp"] if openmp else [])],
                        check=True)
     return out
+
+
+JIT_CACHE = os.path.join(_PKG, "jit_cache")
+
+#: geometries whose run-time compiled fused instance build() prebuilds into
+#: JIT_CACHE (the legal parameter sets tests/test_generic_gpu.py exercises)
+JIT_PREBUILD = (
+    dict(bx=2),
+    dict(kz=3, mhat=(4, 4, 3)),
+    dict(ky=3, by=2, mhat=(4, 3, 2)),
+    dict(kx=1, ky=1, kz=1, bx=0, by=0, mhat=(1, 1, 1), lag_grid_x=(-0.5, 0.0, 0.5), lag_grid_y=(-1.0, 0.0, 1.0)),
+    dict(kx=2, ky=3, kz=1, bx=1, by=2, mhat=(0, 1, 0)),
+)
+
+
+def prebuild_jit(param_sets=JIT_PREBUILD, cache_dir: str = JIT_CACHE) -> None:
+    """NVRTC-compile the fused instances of ``param_sets`` into ``cache_dir``
+    (cubins the library finds at run time; NVRTC needs no GPU)."""
+    import concurrent.futures as cf
+
+    from .params import FilterParams
+
+    lib = load()
+    os.makedirs(cache_dir, exist_ok=True)
+
+    def one(kw):
+        cp, keep = make_params(FilterParams(**kw))
+        rc = lib.cw_jit_prebuild(ctypes.byref(cp), cache_dir.encode())
+        if rc != CW_OK:
+            raise NativeError(f"JIT prebuild {kw}: {(lib.cw_last_error(None) or b'').decode()}")
+
+    with cf.ThreadPoolExecutor(max_workers=max(1, min(len(param_sets), os.cpu_count() or 1))) as ex:
+        list(ex.map(one, param_sets))
 
 
 class cw_scene(ctypes.Structure):
@@ -156,6 +190,8 @@ def load():
         "cw_frames_seen": (i64, [vp]),
         "cw_index_bytes": (i32, [vp]),
         "cw_is_generic": (i32, [vp]),
+        "cw_kernel_kind": (i32, [vp]),
+        "cw_jit_prebuild": (ctypes.c_int, [P(cw_params), ctypes.c_char_p]),
         "cw_read_view": (ctypes.c_int, [vp, i32, vp, ctypes.c_size_t]),
         "cw_launch_info": (ctypes.c_int, [vp, P(i32), P(i32), P(i32), P(i32)]),
         "cw_set_timing": (ctypes.c_int, [vp, i32]),

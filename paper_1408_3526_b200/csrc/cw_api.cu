@@ -8,6 +8,7 @@
 // or the call fails with CW_ERR_CUDA.
 #include "cw_inst.cuh"
 #include "cw_generic.cuh"
+#include "cw_jit.cuh"
 #include "../../include/cw_b200.h"
 
 #ifdef _OPENMP
@@ -92,6 +93,7 @@ struct cw_handle {
     // compiled fused instance; velocity indices are uint16 pairs when a lag
     // grid has more than 256 entries
     bool generic = false;
+    int kind = 0;  // 0: compiled fused instance, 1: run-time compiled fused instance, 2: runtime-geometry kernels
     int idx_bytes = 1;
     GenTables gt{};
     void *d_gtab = nullptr;
@@ -551,9 +553,20 @@ int cw_create(const cw_params *p, int32_t width, int32_t height, int32_t device,
     // lag grids fit its tables; the runtime-geometry path otherwise (or when
     // CW_FORCE_GENERIC=1, for testing it on the compiled geometries)
     LaunchFn fn{};
-    const char *force = std::getenv("CW_FORCE_GENERIC");
-    const bool generic = (force && force[0] == '1') || p->n_lag_x > MAXL || p->n_lag_y > MAXL ||
-                         !find_inst(p->kx, p->ky, p->kz, p->bx, p->by, nl_sym, &fn);
+    const char *force = std::getenv("CW_FORCE_GENERIC"), *nojit = std::getenv("CW_NO_JIT");
+    const bool force_generic = force && force[0] == '1';
+    int kind = 0;
+    bool have = !force_generic && p->n_lag_x <= MAXL && p->n_lag_y <= MAXL &&
+                find_inst(p->kx, p->ky, p->kz, p->bx, p->by, nl_sym, &fn);
+    if (!have && !force_generic && !(nojit && nojit[0] == '1') &&
+        jit_supported(p->kx, p->ky, p->kz, p->bx, p->by, p->n_lag_x, p->n_lag_y)) {
+        std::string jerr;  // no NVRTC / compile failure: the runtime-geometry kernels run instead
+        have = jit_instance(p->kx, p->ky, p->kz, p->bx, p->by, nl_sym, &fn, &jerr);
+        kind = 1;
+    }
+    const bool generic = !have;
+    if (generic)
+        kind = 2;
     const int nret_expect = (2 * p->kz + 1) * (2 * p->bx + 1) * (2 * p->by + 1);
     if (n_retained != nret_expect || !bank_c64 || !retained)
         return fail(nullptr, CW_ERR_VALUE, "bank does not match the retained band of these parameters");
@@ -585,6 +598,7 @@ int cw_create(const cw_params *p, int32_t width, int32_t height, int32_t device,
     h->lag_y.assign(p->lag_y, p->lag_y + p->n_lag_y);
     h->fn = fn;
     h->generic = generic;
+    h->kind = kind;
     h->idx_bytes = (h->nlx > 256 || h->nly > 256) ? 2 : 1;
     std::vector<float> coef;
     if (!generic) {
@@ -740,6 +754,29 @@ int32_t cw_index_bytes(const cw_handle *h) { return h ? h->idx_bytes : -1; }
 
 int32_t cw_is_generic(const cw_handle *h) { return h ? (h->generic ? 1 : 0) : -1; }
 
+int32_t cw_kernel_kind(const cw_handle *h) { return h ? h->kind : -1; }
+
+int cw_jit_prebuild(const cw_params *p, const char *dir)
+{
+    if (!p || !dir)
+        return fail(nullptr, CW_ERR_VALUE, "null argument");
+    auto sym = [](const double *g, int n) {
+        if (n % 2 == 0 || g[n / 2] != 0.0)
+            return false;
+        for (int i = 0; i < n / 2; i++)
+            if (g[i] != -g[n - 1 - i])
+                return false;
+        return true;
+    };
+    const int nl = (p->n_lag_x == p->n_lag_y && sym(p->lag_x, p->n_lag_x) && sym(p->lag_y, p->n_lag_y)) ? p->n_lag_x : 0;
+    if (!jit_supported(p->kx, p->ky, p->kz, p->bx, p->by, p->n_lag_x, p->n_lag_y))
+        return fail(nullptr, CW_ERR_UNSUPPORTED, "geometry beyond the fused kernel (runtime-geometry path)");
+    std::string err;
+    if (jit_prebuild(p->kx, p->ky, p->kz, p->bx, p->by, nl, dir, &err) != 0)
+        return fail(nullptr, CW_ERR_UNSUPPORTED, err);
+    return CW_OK;
+}
+
 int cw_next_frame_slot(cw_handle *h, float **slot)
 {
     if (!h || !slot)
@@ -874,11 +911,22 @@ static int run_frame(cw_handle *h, cudaStream_t s, int32_t *ready, int64_t *fram
         na.NXB = h->NXB;
         na.y_begin = h->halo;
         na.y_off = h->row_off;
-        h->fn.launch_naive(na, h->tab, h->naive_grid, s);
+        if (h->fn.launch_naive) {
+            h->fn.launch_naive(na, h->tab, h->naive_grid, s);
+        } else {
+            void *args[] = {&na, &h->tab};
+            CW_CUDA(h, cudaLaunchKernel(h->fn.naive_kernel, dim3(h->naive_grid), dim3(h->fn.threads), args,
+                                        h->fn.naive_smem, s));
+        }
         CW_CUDA(h, cudaGetLastError());
     }
     if (!h->generic) {
-        h->fn.launch(a, h->tab, h->grid, s);
+        if (h->fn.launch) {
+            h->fn.launch(a, h->tab, h->grid, s);
+        } else {  // run-time compiled instance
+            void *args[] = {&a, &h->tab};
+            CW_CUDA(h, cudaLaunchKernel(h->fn.kernel, dim3(h->grid), dim3(h->fn.threads), args, h->fn.smem, s));
+        }
         CW_CUDA(h, cudaGetLastError());
     }
     if (h->timing)

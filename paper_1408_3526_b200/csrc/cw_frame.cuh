@@ -33,10 +33,27 @@
 // stores and overwrites the staged copy in place with the Hann-conditioned
 // spectrum that the neighbouring rows need.  Per row: 4 CTA barriers.
 #pragma once
+#ifdef __CUDACC_RTC__
+// run-time compiled (NVRTC, cw_jit.cu): no host headers, libcu++ instead
+#include <cuda/std/cstdint>
+#include <cuda/std/type_traits>
+typedef cuda::std::uint8_t uint8_t;
+typedef cuda::std::uint16_t uint16_t;
+typedef cuda::std::uint32_t uint32_t;
+typedef cuda::std::uint64_t uint64_t;
+typedef cuda::std::int64_t int64_t;
+namespace std {
+using cuda::std::integral_constant;
+}
+#ifndef INFINITY
+#define INFINITY __int_as_float(0x7f800000)
+#endif
+#else
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include <type_traits>
+#endif
 
 namespace cwb {
 
@@ -65,6 +82,11 @@ constexpr int RESTART = CW_RESTART;  // rows between direct y-SDFT restarts (bou
 // (an L2 hit; z+ = conj(w) z, conj(w) folded into the coefficients on the
 // host) instead of a 32 KB retained-z+ stage in shared memory
 #define CW_PEF_L2 0
+#endif
+#ifndef CW_TBULK
+// T^ write-back as one TMA bulk store of the smoothed T^ stage (issued after
+// barrier 2 by the issuing thread) instead of per-warp STG
+#define CW_TBULK 0
 #endif
 #ifndef CW_FENCE_ALL
 #define CW_FENCE_ALL 1  // every thread orders its generic stage reads before the next TMA write
@@ -225,6 +247,30 @@ struct Geo {
     static constexpr int MINB = MINB_SMEM < 1 ? 1 : (MINB_SMEM > 3 ? 3 : MINB_SMEM);
 };
 
+// The sizes of Geo<kx, ky, kz, bx, by> as runtime values (for geometries
+// compiled at run time, cw_jit.cu); make_inst checks them against Geo for
+// every compiled instance.
+struct GeoSizes {
+    int threads, nsp, ntp, retpp;
+    unsigned long long smem, naive_smem;
+};
+__host__ __device__ constexpr GeoSizes geo_sizes(int kx, int ky, int kz, int bx, int by)
+{
+    const int mx = 2 * kx + 1, my = 2 * ky + 1, mz = 2 * kz + 1, wx = 2 * bx + 1;
+    const int nr = ky + 1;
+    const int row0p = (kz + 1) + kx * mz, rownp = mx * mz;
+    const int nsp = row0p + ky * rownp;
+    const int ntp = (kx + 1) + ky * mx;
+    const int prow0p = (kz + 1) + bx * mz, prownp = wx * mz;
+    const int retpp = 2 * ((prow0p + 1) / 2 + by * ((prownp + 1) / 2));
+    const unsigned long long smem = (unsigned long long)nsp * 256 + (unsigned long long)ntp * 256 +
+                                    (CW_PEF_L2 ? 0ull : (unsigned long long)retpp * 256) +
+                                    (unsigned long long)(my + 2) * mx * 128 + nr * 256 + (by + 1) * 128 +
+                                    ((MAXL * MAXL * 4) + 15) / 16 * 16 + ((32 + mx - 1) * 4 + 15) / 16 * 16 + 128 + 16;
+    const unsigned long long naive = 4ull * (mz * my * (32 + mx - 1) + mz * my * mx * 32);
+    return GeoSizes{32 * nr, nsp, ntp, retpp, smem, naive};
+}
+
 struct cf {
     float r, i;
 };
@@ -380,6 +426,17 @@ __device__ __forceinline__ void st_state(float2 *p, float2 v)
 
 __device__ __forceinline__ float4 ldg_coef4(const float4 *p) { return __ldg(p); }
 
+// TMA bulk store shared -> global (bulk_group), its commit and the wait for
+// the shared-memory source to be read (the buffer may be overwritten then)
+__device__ __forceinline__ void tma_store(void *dst, const void *src, uint32_t bytes)
+{
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_addr(src)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_store_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void tma_store_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+
 // 4-byte cp.async (LDGSTS) with zero fill when !valid (src-size 0)
 __device__ __forceinline__ void cp_async4(void *dst, const float *src, bool valid)
 {
@@ -461,6 +518,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
     auto issue_t = [&](int yy, int xb) {
         if (use_that && threadIdx.x == ISSUER) {
             const size_t pix = CW_L2ONLY ? (size_t)blockIdx.x : (size_t)yy * NXB + xb;
+            if (CW_TBULK) tma_store_wait_read();  // the T^ store has read the stage
             fence_proxy_async();
             mbar_expect_tx(bar_t, G::SM_TSTAGE);
             tma_load(tstage, a.that + pix * G::NTP * 32, G::SM_TSTAGE, bar_t);
@@ -602,7 +660,13 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                 if (!CW_PEF_L2) sret[q * 32 + lane] = f2(v);
             };
             cf cz[MX][MZ];  // 4 x Hz(z+) per kx column
-            if (CW_MEMONLY) {  // diagnostic: the same HBM traffic, no arithmetic
+            if (CW_MEMONLY == 2) {  // diagnostic: the same traffic, state written back by one bulk store
+                if (threadIdx.x == ISSUER) {
+                    tma_store(a.state + pix * G::NSP * 32, stage, G::SM_STAGE);
+                    tma_store_commit();
+                    tma_store_wait_read();
+                }
+            } else if (CW_MEMONLY) {  // diagnostic: the same HBM traffic, no arithmetic
                 const int np = r == 0 ? G::ROW0P : G::ROWNP;
                 for (int j = 0; j < np; j++) st_state(&stg[j * 32], sst[j * 32]);
             } else if (r == 0) {
@@ -714,6 +778,9 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
             }
             if (CW_FENCE_ALL && !a.ready) fence_proxy_async();  // stage reads before the next TMA write
             CW_STAMP(3);  // observer + Hz + Hx
+            // the previous row's T^ bulk store has read the stage before C1
+            // overwrites it (first ready frame: no T^ load orders it)
+            if (CW_TBULK && threadIdx.x == ISSUER) tma_store_wait_read();
             __syncthreads();  // (1) Cx rows visible; x stage of yy+1 done
             CW_STAMP(4);  // barrier 1 wait
             if (!a.ready) {
@@ -745,7 +812,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                         const float2 o = tstage[j * 32 + lane];
                         v2 = cfma2(cf{t.beta, t.beta}, v2, cmul2(cf{t.alpha, t.alpha}, c2(o)));
                     }
-                    st_state(&thg[j * 32], f2(v2));
+                    if (!CW_TBULK) st_state(&thg[j * 32], f2(v2));
                     tstage[j * 32 + lane] = f2(v2);
                 };
                 // 4^3 x the Hann-conditioned power, collapsed over kz with a_z
@@ -764,7 +831,13 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
 #pragma unroll
                     for (int kzi = 0; kzi < MZ; kzi++) dst[kzi] = cconj(src[MZ - 1 - kzi]);
                 };
-                if (CW_MEMONLY) {
+                if (CW_MEMONLY == 2) {
+                    if (threadIdx.x == ISSUER) {
+                        tma_store(thg - lane, tstage, G::SM_TSTAGE);
+                        tma_store_commit();
+                        tma_store_wait_read();
+                    }
+                } else if (CW_MEMONLY) {
                     const int np = r == 0 ? G::TROW0P : G::TROWNP;
                     for (int j = 0; j < np; j++) {
                         const float2 v = tstage[(G::tpair(r) + j) * 32 + lane];
@@ -830,6 +903,10 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
             __syncthreads();  // (2) T^ rows visible; the state stage is free
             CW_STAMP(6);  // barrier 2 wait
             if (yy + 1 < ye) issue(yy + 1, xb);
+            if (CW_TBULK && !CW_MEMONLY && threadIdx.x == ISSUER) {  // the new T^ packet to HBM
+                tma_store(a.that + pix * G::NTP * 32, tstage, G::SM_TSTAGE);
+                tma_store_commit();
+            }
 
             // ---------------- phase CD: lag contraction + partial argmax ----------------
             // score(ly, lx) = gy gx R^(ly, lx); stage 1 along kx (B(ky, lx)) for
@@ -1136,6 +1213,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
         }
         u += ye - ys;
     }
+    if (CW_TBULK && threadIdx.x == ISSUER) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 #ifdef CW_PHASE_TIMING
     if (blockIdx.x == 0 && (threadIdx.x & 31) == 0)
         for (int k = 0; k < 11; k++) cw_phase_clk[threadIdx.x >> 5][k] += clk_acc[k];

@@ -7,6 +7,8 @@
 namespace cwb {
 
 struct LaunchFn {
+    // compiled instances: launch / launch_naive; run-time compiled ones
+    // (cw_jit.cu): launch == nullptr, kernel / naive_kernel are cudaKernel_t
     void (*launch)(const FrameArgs &, const Tables &, int grid, cudaStream_t);
     void (*launch_naive)(const NaiveArgs &, const Tables &, int grid, cudaStream_t);
     const void *naive_kernel;
@@ -69,6 +71,10 @@ template <int KX, int KY, int KZ, int BX, int BY, int NL>
 LaunchFn make_inst()
 {
     using G = Geo<KX, KY, KZ, BX, BY>;
+    constexpr GeoSizes gs = geo_sizes(KX, KY, KZ, BX, BY);
+    static_assert(gs.threads == G::NTHREADS && gs.nsp == G::NSP && gs.ntp == G::NTP && gs.retpp == G::RETPP &&
+                      gs.smem == G::SMEM_BYTES && gs.naive_smem == naive_smem_bytes<G>(),
+                  "geo_sizes() must mirror Geo");
     LaunchFn f{};
     f.launch = &launch_inst<KX, KY, KZ, BX, BY, NL>;
     if constexpr (NL == 0) {  // one naive kernel per geometry (in the NL = 0 unit)

@@ -91,3 +91,28 @@ def test_compiled_instances_cover_the_benchmarked_geometries():
     out = subprocess.run(["cuobjdump", "-sass", _native.LIB_PATH], capture_output=True, text=True).stdout
     kernels = set(re.findall(r"Function : (_ZN3cwb15cw_frame_kernel\S+)", out))
     assert len(kernels) == len(inst)
+
+
+def test_nvrtc_compiles_a_non_compiled_geometry(tmp_path):
+    """cw_jit_prebuild: NVRTC compiles the fused kernel for a legal geometry
+    that has no instance in the library (no GPU needed) into a cubin cache
+    entry; a geometry beyond the fused kernel's limits is refused (it runs on
+    the runtime-geometry kernels)."""
+    from paper_1408_3526_b200 import FilterParams
+
+    lib = _native.load()
+    cp, keep = _native.make_params(FilterParams(kx=3, ky=2, kz=1, bx=1, by=1, mhat=(3, 2, 1),
+                                                lag_grid_x=(-1.0, 0.0, 1.0), lag_grid_y=(-1.0, 0.0, 1.0)))
+    assert lib.cw_jit_prebuild(ctypes.byref(cp), str(tmp_path).encode()) == _native.CW_OK
+    files = list(tmp_path.glob("g3_2_1_1_1_nl3_*.cubin"))
+    assert len(files) == 1 and files[0].stat().st_size > 10000
+    assert files[0].read_bytes().startswith(b"cw_b200_jit 1\n_ZN3cwb15cw_frame_kernelINS_3GeoILi3ELi2ELi1ELi1ELi1EEELi3EEE")
+    cp, keep = _native.make_params(FilterParams(kx=6, ky=6, bx=5, by=5, mhat=(6, 6, 2)))
+    assert lib.cw_jit_prebuild(ctypes.byref(cp), str(tmp_path).encode()) == _native.CW_ERR_UNSUPPORTED
+
+
+def test_prebuilt_jit_cubins_ship_with_the_tree():
+    """build() leaves the NVRTC cubins of the tested non-compiled geometries
+    in paper_1408_3526_b200/jit_cache (they travel to the GPU box)."""
+    names = {p.name.split("_nl")[0] for p in __import__("pathlib").Path(_native.JIT_CACHE).glob("*.cubin")}
+    assert {"g4_4_2_2_3", "g4_4_3_3_3", "g4_3_2_3_2", "g1_1_1_0_0", "g2_3_1_1_2"} <= names

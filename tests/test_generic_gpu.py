@@ -1,14 +1,16 @@
 """Every validate-legal FilterParams runs on the device (params.py:114-158;
 SPEC.md:69 makes the geometry runtime configuration).
 
-Parameters with a compiled fused instance run the fused kernel; every
-other legal set -- any half window / bandwidth, asymmetric windows, any lag
-grid (odd or even, asymmetric, more than 33 or more than 256 entries) --
-runs the runtime-geometry kernels (csrc/cw_generic.cu).  Both are checked
+Three device paths cover the domain: the fused instances compiled into the
+library (kind 0); the same fused kernel compiled at run time by NVRTC for
+any other geometry within its limits (kind 1: half windows <= 5, lag grids
+<= 33 entries; cubins cached, csrc/cw_jit.cu); and the runtime-geometry
+kernels (kind 2, csrc/cw_generic.cu) for everything else -- larger windows,
+longer lag grids (more than 256 entries: uint16 indices).  Each is checked
 against the float64 oracle / the reference's golden vectors with the
-tolerances of tests/parity.py.  CW_FORCE_GENERIC=1 routes the compiled
-geometries through the runtime-geometry path too, so the two device paths
-are also compared with each other."""
+tolerances of tests/parity.py.  CW_NO_JIT=1 sends the kind-1 geometries to
+the runtime-geometry kernels and CW_FORCE_GENERIC=1 the compiled ones, so
+all paths are compared on the same parameter sets."""
 
 import numpy as np
 import pytest
@@ -42,13 +44,20 @@ def _check(params, frames, gpu_outs, ref_outs):
 
 
 def _run(params, frames, **kw):
+    """(outputs, ran the runtime-geometry kernels)"""
+    outs, kind = _run_kind(params, frames, **kw)
+    return outs, kind == 2
+
+
+def _run_kind(params, frames, **kw):
     from paper_1408_3526_b200 import Pipeline, _native
 
     t, h, w = frames.shape
     with Pipeline(params, w, h, **kw) as pipe:
         outs = [o for o in map(pipe.process_frame, frames) if o is not None]
-        generic = bool(_native.load().cw_is_generic(pipe._h))
-    return outs, generic
+        kind = int(_native.load().cw_kernel_kind(pipe._h))
+        assert bool(_native.load().cw_is_generic(pipe._h)) == (kind == 2)
+    return outs, kind
 
 
 def _oracle(params, frames, forced=None):
@@ -73,7 +82,8 @@ def test_generic_path_on_the_golden_cases(name, monkeypatch):
 
 
 LEGAL = {
-    # (kx, ky, kz, bx, by, mhat, lag_x, lag_y): none has a compiled instance
+    # (kx, ky, kz, bx, by, mhat, lag_x, lag_y): none has an instance compiled
+    # into the library
     "bx2": (4, 4, 2, 2, 3, (4, 4, 2), None, None),
     "kz3": (4, 4, 3, 3, 3, (4, 4, 3), None, None),
     "ky3_by2": (4, 3, 2, 3, 2, (4, 3, 2), None, None),
@@ -100,16 +110,40 @@ def _params(spec):
     return p
 
 
+# kind each set runs with NVRTC available: beyond the fused kernel's limits
+# (K = 6, 41 lags) -> runtime-geometry kernels; a short lag grid on the
+# compiled default geometry -> the compiled runtime-loop instance
+EXPECTED_KIND = {"k6": 2, "lags41_asym": 2, "lags_even": 0}
+
+
+@pytest.mark.parametrize("path", ["fused", "runtime_geometry"])
 @pytest.mark.parametrize("name", sorted(LEGAL))
-def test_legal_geometry_matches_oracle(name):
+def test_legal_geometry_matches_oracle(name, path, monkeypatch):
+    if path == "runtime_geometry":
+        monkeypatch.setenv("CW_NO_JIT", "1")
     p = _params(LEGAL[name])
     h, w = 2 * p.my + 22, 2 * p.mx + 31
     frames = _frames(p.mz + 7, h, w, seed=len(name))
-    outs, generic = _run(p, frames)
-    # no compiled instance: the runtime-geometry path ran (a short lag grid on
-    # a compiled geometry runs the fused kernel's runtime-loop instance)
-    assert generic == (name != "lags_even")
+    outs, kind = _run_kind(p, frames)
+    want = EXPECTED_KIND.get(name, 1)
+    assert kind == (2 if path == "runtime_geometry" and want == 1 else want)
     _check(p, frames, outs, _oracle(p, frames))
+
+
+def test_jit_instance_equals_generic_on_the_same_geometry(monkeypatch):
+    """The run-time compiled fused kernel and the runtime-geometry kernels on
+    one non-compiled geometry: the same velocities up to near-ties."""
+    p = _params(LEGAL["kz3"])
+    frames = _frames(14, 60, 72, seed=12)
+    fused, k1 = _run_kind(p, frames)
+    monkeypatch.setenv("CW_NO_JIT", "1")
+    gen, k2 = _run_kind(p, frames)
+    assert (k1, k2) == (1, 2)
+    fmax = float(np.abs(frames).max())
+    for a, b in zip(fused, gen):
+        assert velocity_agreement(a.velocity.indices, b.velocity.indices, p) >= VEL_FRAC
+        m = a.mask & agreeing_outputs(a.velocity.indices, b.velocity.indices, p)
+        assert residual_error(a.residual, b.residual.astype(np.float64), m, fmax) <= RES_TOL
 
 
 def test_more_than_256_lags_use_16_bit_indices():
@@ -171,14 +205,18 @@ def test_generic_equals_fused_on_the_default_geometry(params, monkeypatch):
         assert residual_error(a.residual, b.residual.astype(np.float64), m, fmax) <= RES_TOL
 
 
-def test_generic_naive_backend_forced_velocity_and_detection():
-    """The runtime path's naive spectrum backend, forced velocity and the
-    fused detection metrics (pipeline.py:139-142, 174-177, 260-265)."""
+@pytest.mark.parametrize("path", ["fused", "runtime_geometry"])
+def test_generic_naive_backend_forced_velocity_and_detection(path, monkeypatch):
+    """The naive spectrum backend, forced velocity and the detection metrics
+    (pipeline.py:139-142, 174-177, 260-265) on a non-compiled geometry, run
+    time compiled and on the runtime-geometry kernels."""
+    if path == "runtime_geometry":
+        monkeypatch.setenv("CW_NO_JIT", "1")
     p = _params(LEGAL["kz3"])
     frames = _frames(11, 40, 44, seed=4)
     ref = _oracle(p, frames)
-    outs, generic = _run(p, frames, spectrum_backend="naive", detect_threshold=0.05)
-    assert generic
+    outs, kind = _run_kind(p, frames, spectrum_backend="naive", detect_threshold=0.05)
+    assert kind == (1 if path == "fused" else 2)
     _check(p, frames, outs, ref)
     for o in outs:
         want = np.sqrt(np.mean(o.residual[o.mask].astype(np.float64) ** 2))
@@ -190,8 +228,12 @@ def test_generic_naive_backend_forced_velocity_and_detection():
     assert np.all(outs[-1].velocity.indices == (2, 5))
 
 
-def test_generic_strips_stitch_to_the_full_frame():
-    """Strip sharding (halo rows + row offset, strips.py) on the runtime path."""
+@pytest.mark.parametrize("path", ["fused", "runtime_geometry"])
+def test_generic_strips_stitch_to_the_full_frame(path, monkeypatch):
+    """Strip sharding (halo rows + row offset, strips.py) on a non-compiled
+    geometry, both paths."""
+    if path == "runtime_geometry":
+        monkeypatch.setenv("CW_NO_JIT", "1")
     import torch
 
     from paper_1408_3526_b200 import Pipeline
@@ -216,9 +258,13 @@ def test_generic_strips_stitch_to_the_full_frame():
                                               g.residual[pl.lo + r0:pl.a1 - mhy])
 
 
-def test_generic_snapshot_and_views(monkeypatch):
-    """Checkpoint / resume and the spectrum / T^ parity views on the runtime
-    path (the spectrum against the oracle's, per pixel)."""
+@pytest.mark.parametrize("path", ["fused", "runtime_geometry"])
+def test_generic_snapshot_and_views(path, monkeypatch):
+    """Checkpoint / resume and the spectrum / T^ parity views on a
+    non-compiled geometry, both paths (the spectrum against the oracle's,
+    per pixel)."""
+    if path == "runtime_geometry":
+        monkeypatch.setenv("CW_NO_JIT", "1")
     from oracle.oracle import OraclePipeline
     from paper_1408_3526_b200 import Pipeline
     from parity import SPEC_TOL, per_pixel_rel
