@@ -458,6 +458,13 @@ C5_SWEEP = {
 }
 
 
+JIT_SWEEP = {
+    "(4,4,3,3,3) lag 1/4": dict(kz=3, mhat=(4, 4, 3)),
+    "(4,4,2,2,3) lag 1/4": dict(bx=2),
+    "(4,3,2,3,2) lag 1/4": dict(ky=3, by=2, mhat=(4, 3, 2)),
+}
+
+
 def _device_run(lib, pipe, frames, steps, warmup, stream, dist=None, before_push=None):
     """Time `steps` device-resident pushes on `stream` (CUDA events, barrier
     on both sides) after the temporal window and `warmup` frames; returns
@@ -567,6 +574,26 @@ def run_config(args):
                 el, kern, n, clk = _device_run(lib, pipe, frames, args.steps, args.warmup, stream, dist)
             line("pixel-frames/sec (1280x1024 stream per GPU, params sweep)", f"C5: {name}", w * h * world, p, el,
                  kern, n, clk, "weak", {"frame": [w, h], "streams": world, "params": name})
+    elif args.config == "jit":
+        # legal geometries with no instance in the library: the
+        # fused kernel compiled at run time (NVRTC) vs the runtime-geometry
+        # kernels, 1280x1024
+        w, h = 1280, 1024
+        frames = generate_device(SimConfig(width=w, height=h, frame_count=1000, rng_seed=rank), device=dev,
+                                 frames=16)
+        for name, kw in JIT_SWEEP.items():
+            p = FilterParams(**kw)
+            for path in ("fused (run-time compiled)", "runtime-geometry kernels"):
+                if path.startswith("runtime"):
+                    os.environ["CW_NO_JIT"] = "1"
+                with Pipeline(p, w, h, device=local) as pipe:
+                    kind = int(lib.cw_kernel_kind(pipe._h))
+                    steps = args.steps if kind != 2 else max(3, min(args.steps, 30))
+                    el, kern, n, clk = _device_run(lib, pipe, frames, steps, args.warmup, stream, dist)
+                os.environ.pop("CW_NO_JIT", None)
+                line("pixel-frames/sec (1280x1024, geometry without a compiled instance)", f"{name}: {path}",
+                     w * h * world, p, el * args.steps / steps, kern, n, clk, "weak",
+                     {"frame": [w, h], "params": name, "kernel_kind": kind})
     elif args.config == "c3naive":
         # the paper's naive-vs-recursive comparison at 640x512
         p = default_params()
@@ -680,7 +707,7 @@ def main():
     ap.add_argument("--c4-steps", type=int, default=400, help="timed frames of the C4 block (capped by --steps)")
     ap.add_argument("--ref-budget", type=float, default=60.0,
                     help="--impl reference: seconds of timed CPU work (steps are capped to fit)")
-    ap.add_argument("--config", choices=("c3", "c2", "c4", "c4strips", "c5", "c3naive", "c3seq"), default="c3",
+    ap.add_argument("--config", choices=("c3", "c2", "c4", "c4strips", "c5", "c3naive", "c3seq", "jit"), default="c3",
                     help="c3 (default, the headline) or another BASELINE.json configuration")
     args = ap.parse_args()
     if args.warmup < 3:
