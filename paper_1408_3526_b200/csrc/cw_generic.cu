@@ -114,32 +114,37 @@ __global__ void __launch_bounds__(128) gen_flow(const GenArgs a, const GenTables
             return a.state[((size_t)(kz * a.my + ky) * a.mx + kx) * HW + p];
         };
         const float hw[3] = {-0.25f, 0.5f, -0.25f};
+        // hann3 (_kernels.py:177-217) is separable: G(kz') = (Hy Hx C)(kz', ky, kx)
+        // from 9 taps, then Hz over a rolling window G(kz-1), G(kz), G(kz+1)
+        auto gxy = [&](int kz, int ky, int kx) -> float2 {
+            float2 sy = make_float2(0.f, 0.f);
+            for (int dy = 0; dy < 3; dy++) {
+                const int iy = wrap(ky + dy - 1, a.my);
+                float2 sx = make_float2(0.f, 0.f);
+                for (int dx = 0; dx < 3; dx++) {
+                    const float2 c = cond(kz, iy, wrap(kx + dx - 1, a.mx));
+                    sx.x += hw[dx] * c.x;
+                    sx.y += hw[dx] * c.y;
+                }
+                sy.x += hw[dy] * sx.x;
+                sy.y += hw[dy] * sx.y;
+            }
+            return sy;
+        };
         for (int ky = 0; ky < a.my; ky++)
             for (int kx = 0; kx < a.mx; kx++) {
                 float2 tz = make_float2(0.f, 0.f);
+                const float2 glast = gxy(a.mz - 1, ky, kx), gfirst = gxy(0, ky, kx);
+                float2 gm = glast, g0 = gfirst;
                 for (int kz = 0; kz < a.mz; kz++) {
-                    // hann3 (_kernels.py:177-217) as its 27-point circular stencil
-                    float2 hsum = make_float2(0.f, 0.f);
-                    for (int dz = 0; dz < 3; dz++) {
-                        const int iz = wrap(kz + dz - 1, a.mz);
-                        float2 sy = make_float2(0.f, 0.f);
-                        for (int dy = 0; dy < 3; dy++) {
-                            const int iy = wrap(ky + dy - 1, a.my);
-                            float2 sx = make_float2(0.f, 0.f);
-                            for (int dx = 0; dx < 3; dx++) {
-                                const float2 c = cond(iz, iy, wrap(kx + dx - 1, a.mx));
-                                sx.x += hw[dx] * c.x;
-                                sx.y += hw[dx] * c.y;
-                            }
-                            sy.x += hw[dy] * sx.x;
-                            sy.y += hw[dy] * sx.y;
-                        }
-                        hsum.x += hw[dz] * sy.x;
-                        hsum.y += hw[dz] * sy.y;
-                    }
-                    const float pw = hsum.x * hsum.x + hsum.y * hsum.y;  // power (_kernels.py:220-227)
+                    const float2 gp = kz + 1 < a.mz ? (kz + 1 == a.mz - 1 ? glast : gxy(kz + 1, ky, kx)) : gfirst;
+                    const float2 h = make_float2(hw[0] * gm.x + hw[1] * g0.x + hw[2] * gp.x,
+                                                 hw[0] * gm.y + hw[1] * g0.y + hw[2] * gp.y);
+                    const float pw = h.x * h.x + h.y * h.y;  // power (_kernels.py:220-227)
                     tz.x += t.az[kz].x * pw;
                     tz.y += t.az[kz].y * pw;
+                    gm = g0;
+                    g0 = gp;
                 }
                 float2 *th = a.that + (size_t)(ky * a.mx + kx) * HW + p;
                 if (a.first) {
@@ -149,16 +154,32 @@ __global__ void __launch_bounds__(128) gen_flow(const GenArgs a, const GenTables
                     *th = make_float2(a.beta * tz.x + a.alpha * o.x, a.beta * tz.y + a.alpha * o.y);
                 }
             }
-        // R(ly, lx) = Re sum_ky ayl sum_kx axl T^ (gains folded); total-order argmax
+        // R(ly, lx) = Re sum_ky ayl(ly) B(ky, lx), B = sum_kx axl(lx) T^ (gains
+        // folded; the separable order of _kernels.py:230-258); total-order argmax
         float best = 0.f;
         uint32_t brank = 0xffffffffu;
-        for (int ly = 0; ly < a.nly; ly++)
-            for (int lx = 0; lx < a.nlx; lx++) {
-                float r = 0.f;
+        constexpr int MAXB = 64;
+        float2 bk[MAXB];
+        for (int lx = 0; lx < a.nlx; lx++) {
+            const bool cache = a.my <= MAXB;
+            if (cache)
                 for (int ky = 0; ky < a.my; ky++) {
                     float2 b = make_float2(0.f, 0.f);
                     for (int kx = 0; kx < a.mx; kx++)
                         b = cadd(b, cmul(t.axl[lx * a.mx + kx], a.that[(size_t)(ky * a.mx + kx) * HW + p]));
+                    bk[ky] = b;
+                }
+            for (int ly = 0; ly < a.nly; ly++) {
+                float r = 0.f;
+                for (int ky = 0; ky < a.my; ky++) {
+                    float2 b;
+                    if (cache) {
+                        b = bk[ky];
+                    } else {
+                        b = make_float2(0.f, 0.f);
+                        for (int kx = 0; kx < a.mx; kx++)
+                            b = cadd(b, cmul(t.axl[lx * a.mx + kx], a.that[(size_t)(ky * a.mx + kx) * HW + p]));
+                    }
                     const float2 e = t.ayl[ly * a.my + ky];
                     r += e.x * b.x - e.y * b.y;
                 }
@@ -168,6 +189,7 @@ __global__ void __launch_bounds__(128) gen_flow(const GenArgs a, const GenTables
                     brank = rk;
                 }
             }
+        }
         vix = t.rix[brank];
         viy = t.riy[brank];
     }
