@@ -124,6 +124,9 @@ def prebuild_jit(param_sets=JIT_PREBUILD, cache_dir: str = JIT_CACHE) -> None:
 
     lib = load()
     os.makedirs(cache_dir, exist_ok=True)
+    for f in os.listdir(cache_dir):  # cubins of older kernel sources
+        if f.endswith(".cubin"):
+            os.unlink(os.path.join(cache_dir, f))
 
     def one(kw):
         cp, keep = make_params(FilterParams(**kw))

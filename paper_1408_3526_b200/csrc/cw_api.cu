@@ -101,6 +101,7 @@ struct cw_handle {
     int nxf = 0;  // x-stage frames allocated
     // fused kernel work split (FrameArgs.work): static fraction + dynamic chunks
     unsigned int *d_work = nullptr;
+    unsigned char *d_rank = nullptr;  // compact instances: rank u16 [nl], then (ix, iy) u8 pairs [nl]
     double dyn_static = 0.92;  // measured on C3 (tools/ab_kernel.py): 0.92 / 2 rows, ~1% faster than all-static
     int dyn_chunk = 2;
     int nslots = 0;  // frame ring slots: max(mhat_z + 2, Mz + 1) (async upload spare; naive window)
@@ -679,6 +680,18 @@ int cw_create(const cw_params *p, int32_t width, int32_t height, int32_t device,
         h->dyn_chunk = std::max(1, std::atoi(e));
     if (cudaMalloc(&h->d_work, 2 * sizeof(unsigned int)) != cudaSuccess)
         return cleanup_fail(CW_ERR_NOMEM, "device allocation failed");
+    if (!generic && fn.compact) {  // the rank tables the compact instance reads from global memory
+        const int nl = h->nlx * h->nly;
+        std::vector<unsigned char> rk((size_t)nl * 4);
+        std::memcpy(rk.data(), h->tab.rank, (size_t)nl * 2);
+        for (int i = 0; i < nl; i++) {
+            rk[(size_t)nl * 2 + 2 * i] = h->tab.rix[i];
+            rk[(size_t)nl * 2 + 2 * i + 1] = h->tab.riy[i];
+        }
+        if (cudaMalloc(&h->d_rank, rk.size()) != cudaSuccess ||
+            cudaMemcpy(h->d_rank, rk.data(), rk.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+            return cleanup_fail(CW_ERR_NOMEM, "device allocation failed");
+    }
     cudaMemsetAsync(h->d_work, 0, 2 * sizeof(unsigned int), h->own);
     if (cudaStreamSynchronize(h->own) != cudaSuccess)
         return cleanup_fail(CW_ERR_CUDA, "device initialisation failed");
@@ -703,6 +716,7 @@ void cw_destroy(cw_handle *h)
     cudaFree(h->d_vidx);
     cudaFree(h->d_gtab);
     cudaFree(h->d_work);
+    cudaFree(h->d_rank);
     cudaFree(h->d_xf);
     cudaFree(h->d_det);
     if (h->h_det)
@@ -838,6 +852,8 @@ static int run_frame(cw_handle *h, cudaStream_t s, int32_t *ready, int64_t *fram
         a.static_units = su < 0 ? 0 : su;
         a.dyn_chunk = h->dyn_chunk;
     }
+    a.rank_g = reinterpret_cast<const uint16_t *>(h->d_rank);
+    a.rxy_g = h->d_rank ? h->d_rank + (size_t)h->nlx * h->nly * 2 : nullptr;
     a.det = nullptr;
     a.det_tau = h->det_tau;
     a.det_cap = h->det_cap;

@@ -153,6 +153,8 @@ struct FrameArgs {
     // L2-slice distance, SM-mate) take fewer chunks, so they all end together
     unsigned int *work;
     int parity;
+    const uint16_t *rank_g;  // compact-mode instances: rank table [nly * nlx] ...
+    const uint8_t *rxy_g;    // ... and rank -> (ix, iy) pairs, in global memory
     long long static_units;
     int dyn_chunk;
     int mhx, mhy;
@@ -222,7 +224,9 @@ struct Geo {
     // loads and (re, im, re, im) retained-z+ quads in shared memory
     static constexpr int PROW0Q = (PROW0P + 1) / 2, PROWNQ = (PROWNP + 1) / 2;  // quads per row
     static constexpr int RETPP = 2 * (PROW0Q + BY * PROWNQ);                    // padded pairs
-    static constexpr int RING = MY + 2;           // x-stage ring rows
+    // x-stage ring rows: yy - MY (comb) .. yy; the next row's x stage reuses
+    // the slot of yy - MY once phase B of yy is past (barrier-ordered)
+    static constexpr int RING = MY + 1;
     static constexpr int XF = MX;                 // x-stage floats per (row, col)
     __host__ __device__ static constexpr int spair(int r) { return r == 0 ? 0 : ROW0P + (r - 1) * ROWNP; }
     __host__ __device__ static constexpr int tpair(int r) { return r == 0 ? 0 : TROW0P + (r - 1) * TROWNP; }
@@ -231,20 +235,37 @@ struct Geo {
     // shared memory plan (bytes)
     static constexpr int SM_STAGE = NSP * 32 * 8;     // state packet -> Cx in place
     static constexpr int SM_TSTAGE = NTP * 32 * 8;    // T^ packet
-    static constexpr int SM_RET = CW_PEF_L2 ? 0 : RETPP * 32 * 8;  // retained z+ quads
+    static constexpr int SM_RET_FULL = RETPP * 32 * 8;  // retained z+ quads
     static constexpr int SM_XF = RING * XF * 32 * 4;  // x-stage ring
     static constexpr int SM_BEST = NR * 32 * 8;       // partial argmax (score, rank)
     static constexpr int SM_PEF = (BY + 1) * 32 * 4;
-    static constexpr int SM_RANK = ((MAXL * MAXL * 4) + 15) / 16 * 16;  // rank u16 + (ix, iy) u8 pairs
+    static constexpr int SM_RANK_FULL = ((MAXL * MAXL * 4) + 15) / 16 * 16;  // rank u16 + (ix, iy) u8 pairs
     static constexpr int SM_ROW = ((32 + MX - 1) * 4 + 15) / 16 * 16;  // next frame row segment
     static constexpr int SM_DEL = 32 * 4;                               // delayed-frame values
     static constexpr int SM_BAR = 16;
-    static constexpr size_t SMEM_BYTES =
-        SM_STAGE + SM_TSTAGE + SM_RET + SM_XF + SM_BEST + SM_PEF + SM_RANK + SM_ROW + SM_DEL + SM_BAR;
+    static constexpr size_t SMEM_BASE = SM_STAGE + SM_TSTAGE + SM_XF + SM_BEST + SM_PEF + SM_ROW + SM_DEL + SM_BAR;
+    // Compact mode: when the full plan keeps the SM at one CTA but dropping
+    // the retained-z+ stage (PEF reads z+ back from the state row in L2,
+    // conj(w) folded into the coefficients) and the smem rank table (read
+    // from global) fits two, the second CTA is worth more than both
+    // (e.g. (4,4,3,3,3): 1.61 -> 1.49 ms per 1280x1024 frame); C3's geometry
+    // already fits two.  Not for KY >= 5: at two CTAs the 168-register cap
+    // spills its contraction ((5,5,2,4,4): 1.55 -> 1.74 ms, measured).
+    static constexpr bool fits2(size_t b) { return 2 * (b + 1024 + 64) <= 228 * 1024; }
+    static constexpr bool COMPACT =
+        KY <= 4 && !fits2(SMEM_BASE + SM_RET_FULL + SM_RANK_FULL) && fits2(SMEM_BASE);
+    static constexpr bool PEF_L2 = CW_PEF_L2 || COMPACT;
+    static constexpr int SM_RET = PEF_L2 ? 0 : SM_RET_FULL;
+    static constexpr int SM_RANK = COMPACT ? 0 : SM_RANK_FULL;
+    static constexpr size_t SMEM_BYTES = SMEM_BASE + SM_RET + SM_RANK;
     // resident CTAs per SM the register budget is sized for: as many as the
     // 228 KB of shared memory hold (1 KB reserved per CTA), at most 3
     static constexpr int MINB_SMEM = (int)((228 * 1024) / (SMEM_BYTES + 1024));
+#ifdef CW_FORCE_MINB  // experiments: the register budget of CW_FORCE_MINB CTAs per SM
+    static constexpr int MINB = CW_FORCE_MINB;
+#else
     static constexpr int MINB = MINB_SMEM < 1 ? 1 : (MINB_SMEM > 3 ? 3 : MINB_SMEM);
+#endif
 };
 
 // The sizes of Geo<kx, ky, kz, bx, by> as runtime values (for geometries
@@ -253,6 +274,7 @@ struct Geo {
 struct GeoSizes {
     int threads, nsp, ntp, retpp;
     unsigned long long smem, naive_smem;
+    int compact, pef_l2;
 };
 __host__ __device__ constexpr GeoSizes geo_sizes(int kx, int ky, int kz, int bx, int by)
 {
@@ -263,12 +285,16 @@ __host__ __device__ constexpr GeoSizes geo_sizes(int kx, int ky, int kz, int bx,
     const int ntp = (kx + 1) + ky * mx;
     const int prow0p = (kz + 1) + bx * mz, prownp = wx * mz;
     const int retpp = 2 * ((prow0p + 1) / 2 + by * ((prownp + 1) / 2));
-    const unsigned long long smem = (unsigned long long)nsp * 256 + (unsigned long long)ntp * 256 +
-                                    (CW_PEF_L2 ? 0ull : (unsigned long long)retpp * 256) +
-                                    (unsigned long long)(my + 2) * mx * 128 + nr * 256 + (by + 1) * 128 +
-                                    ((MAXL * MAXL * 4) + 15) / 16 * 16 + ((32 + mx - 1) * 4 + 15) / 16 * 16 + 128 + 16;
+    const unsigned long long base = (unsigned long long)nsp * 256 + (unsigned long long)ntp * 256 +
+                                    (unsigned long long)(my + 1) * mx * 128 + nr * 256 + (by + 1) * 128 +
+                                    ((32 + mx - 1) * 4 + 15) / 16 * 16 + 128 + 16;
+    const unsigned long long ret = (unsigned long long)retpp * 256, rank = ((MAXL * MAXL * 4) + 15) / 16 * 16;
+    const bool compact =
+        ky <= 4 && !(2 * (base + ret + rank + 1024 + 64) <= 228 * 1024) && 2 * (base + 1024 + 64) <= 228 * 1024;
+    const bool pef_l2 = CW_PEF_L2 || compact;
+    const unsigned long long smem = base + (pef_l2 ? 0 : ret) + (compact ? 0 : rank);
     const unsigned long long naive = 4ull * (mz * my * (32 + mx - 1) + mz * my * mx * 32);
-    return GeoSizes{32 * nr, nsp, ntp, retpp, smem, naive};
+    return GeoSizes{32 * nr, nsp, ntp, retpp, smem, naive, compact ? 1 : 0, pef_l2 ? 1 : 0};
 }
 
 struct cf {
@@ -465,8 +491,8 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
     float *xfr = reinterpret_cast<float *>(smem_raw + G::SM_STAGE + G::SM_TSTAGE + G::SM_RET);
     float2 *pbest = reinterpret_cast<float2 *>(smem_raw + G::SM_STAGE + G::SM_TSTAGE + G::SM_RET + G::SM_XF);
     float *ppef = reinterpret_cast<float *>(reinterpret_cast<unsigned char *>(pbest) + G::SM_BEST);
-    uint16_t *srank = reinterpret_cast<uint16_t *>(reinterpret_cast<unsigned char *>(ppef) + G::SM_PEF);
-    float *rowbuf = reinterpret_cast<float *>(reinterpret_cast<unsigned char *>(srank) + G::SM_RANK);
+    uint16_t *srank_s = reinterpret_cast<uint16_t *>(reinterpret_cast<unsigned char *>(ppef) + G::SM_PEF);
+    float *rowbuf = reinterpret_cast<float *>(reinterpret_cast<unsigned char *>(srank_s) + G::SM_RANK);
     float *delbuf = reinterpret_cast<float *>(reinterpret_cast<unsigned char *>(rowbuf) + G::SM_ROW);
     uint64_t *bar = reinterpret_cast<uint64_t *>(reinterpret_cast<unsigned char *>(delbuf) + G::SM_DEL);
 
@@ -482,11 +508,17 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
     __shared__ long long s_claim;
     const bool use_that = a.ready && !a.first;
 
-    uint8_t *srxy = reinterpret_cast<uint8_t *>(srank + MAXL * MAXL);  // rank -> (ix, iy)
-    for (int i = threadIdx.x; i < nlx * nly; i += G::NTHREADS) {
-        srank[i] = t.rank[i];
-        srxy[2 * i] = t.rix[i];
-        srxy[2 * i + 1] = t.riy[i];
+    // rank table and rank -> (ix, iy): shared memory, or (compact mode) the
+    // copy the host keeps in global memory (L1-cached)
+    const uint16_t *srank = G::COMPACT ? a.rank_g : srank_s;
+    const uint8_t *srxy = G::COMPACT ? a.rxy_g : reinterpret_cast<const uint8_t *>(srank_s + MAXL * MAXL);
+    if (!G::COMPACT) {
+        uint8_t *sxy = reinterpret_cast<uint8_t *>(srank_s + MAXL * MAXL);
+        for (int i = threadIdx.x; i < nlx * nly; i += G::NTHREADS) {
+            srank_s[i] = t.rank[i];
+            sxy[2 * i] = t.rix[i];
+            sxy[2 * i + 1] = t.riy[i];
+        }
     }
     const float2 tw_r = t.tw2[threadIdx.x >> 5], twn_r = t.twn2[threadIdx.x >> 5];  // this warp's y resonator
     uint64_t *bar_t = bar + 1;  // bar: observer-state packet, bar_t: T^ packet
@@ -625,7 +657,6 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
         for (int yy = ys; yy < ye; yy++) {
             // ---------------- phase B: spatial SDFT, observer, Hz, Hx ----------------
             CW_STAMP(0);  // previous row's tail (phase F / loop) -> here
-            if (!a.ready && r == KY && yy + 1 < ye) xstage(yy + 1, x, ring_slot(yy + 1));
             if (((yy - ys) % RESTART) == 0) {
                 // direct restart sum_my e^{+j 2 pi ky my / My} xf(yy - my) (_kernels.py:58-61)
 #pragma unroll
@@ -657,7 +688,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
             // last Mz spatial spectra (_kernels.py:71-90, S = norm * z+).
             // retained z+ (the PEF input), pair q of the padded layout
             auto rput = [&](int q, cf v) {
-                if (!CW_PEF_L2) sret[q * 32 + lane] = f2(v);
+                if (!G::PEF_L2) sret[q * 32 + lane] = f2(v);
             };
             cf cz[MX][MZ];  // 4 x Hz(z+) per kx column
             if (CW_MEMONLY == 2) {  // diagnostic: the same traffic, state written back by one bulk store
@@ -783,9 +814,13 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
             if (CW_TBULK && threadIdx.x == ISSUER) tma_store_wait_read();
             __syncthreads();  // (1) Cx rows visible; x stage of yy+1 done
             CW_STAMP(4);  // barrier 1 wait
-            if (!a.ready) {
-                if (yy + 1 < ye) issue(yy + 1, xb);  // stage free: next row's state
-                    continue;
+            if (!a.ready) {  // warm-up frame: spectrum state only
+                if (yy + 1 < ye) {
+                    issue(yy + 1, xb);  // stage free: next row's state
+                    if (r == KY) xstage(yy + 1, x, ring_slot(yy + 1));  // over slot yy - MY, read in B
+                }
+                __syncthreads();  // the x stage of yy + 1 visible to the next row's phase B
+                continue;
             }
 
             // async prefetches consumed at the end of CD (x stage of yy+1) and in F (residual)
@@ -1164,7 +1199,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                 // retained pair q of row r: smem stage, or the state row in
                 // L2 (row 0: pair q; rows >= 1: pair q + (KX - BX) MZ; the odd
                 // pad pair has a zero coefficient and reads a real pair)
-                const float2 *sr = CW_PEF_L2
+                const float2 *sr = G::PEF_L2
                     ? a.state + ((CW_L2ONLY ? (size_t)blockIdx.x : (size_t)yy * NXB + xb) * G::NSP + G::spair(r) +
                                  (r == 0 ? 0 : (KX - BX) * MZ)) * 32 + lane
                     : sret + 2 * G::pquad(r) * 32 + lane;

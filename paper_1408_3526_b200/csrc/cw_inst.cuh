@@ -18,7 +18,8 @@ struct LaunchFn {
     size_t smem;
     int nsp, ntp, retp;  // float2 pairs per pixel: observer state, T^, retained (PEF rows padded)
     int nl;              // compiled lag count (0: runtime loops)
-    int pef_l2;          // CW_PEF_L2 build: PEF coefficients carry conj(w(kz))
+    int pef_l2;          // PEF reads the stored state: coefficients carry conj(w(kz))
+    int compact;         // rank tables read from global memory (FrameArgs.rank_g / rxy_g)
     void (*phase_clocks)(unsigned long long *dst);  // CW_PHASE_TIMING builds: this unit's clocks
 };
 
@@ -73,7 +74,8 @@ LaunchFn make_inst()
     using G = Geo<KX, KY, KZ, BX, BY>;
     constexpr GeoSizes gs = geo_sizes(KX, KY, KZ, BX, BY);
     static_assert(gs.threads == G::NTHREADS && gs.nsp == G::NSP && gs.ntp == G::NTP && gs.retpp == G::RETPP &&
-                      gs.smem == G::SMEM_BYTES && gs.naive_smem == naive_smem_bytes<G>(),
+                      gs.smem == G::SMEM_BYTES && gs.naive_smem == naive_smem_bytes<G>() &&
+                      gs.compact == (G::COMPACT ? 1 : 0) && gs.pef_l2 == (G::PEF_L2 ? 1 : 0),
                   "geo_sizes() must mirror Geo");
     LaunchFn f{};
     f.launch = &launch_inst<KX, KY, KZ, BX, BY, NL>;
@@ -89,7 +91,8 @@ LaunchFn make_inst()
     f.ntp = G::NTP;
     f.retp = G::RETPP;
     f.nl = NL;
-    f.pef_l2 = CW_PEF_L2;
+    f.pef_l2 = G::PEF_L2 ? 1 : 0;
+    f.compact = G::COMPACT ? 1 : 0;
 #ifdef CW_PHASE_TIMING
     f.phase_clocks = &phase_clocks_read;
 #endif

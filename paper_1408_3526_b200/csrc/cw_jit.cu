@@ -273,7 +273,8 @@ bool jit_instance(int kx, int ky, int kz, int bx, int by, int nl, LaunchFn *out,
     f.ntp = g.ntp;
     f.retp = g.retpp;
     f.nl = nl;
-    f.pef_l2 = CW_PEF_L2;
+    f.pef_l2 = g.pef_l2;
+    f.compact = g.compact;
     g_loaded[file] = f;
     *out = f;
     return true;
