@@ -137,10 +137,25 @@ class ClockSampler:
 
 
 def dist_setup():
+    """(world, rank, CUDA device of this rank).  CW_BENCH_DEVICE pins every
+    rank to one device: the multi-rank code path run on a one-GPU box by
+    the tests (with CW_BENCH_BACKEND=gloo), never a measurement."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("CW_BENCH_DEVICE", os.environ.get("LOCAL_RANK", "0")))
     return world, rank, local
+
+
+def init_dist(local):
+    import torch
+    import torch.distributed as dist
+
+    backend = os.environ.get("CW_BENCH_BACKEND", "nccl")
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend)
+    return dist
 
 
 def cpu_oracle_rate(params, frames_np, budget_s=12.0, threads=None, max_frames=64):
@@ -183,7 +198,7 @@ def run_reference(args):
     p = default_params()
     threads = os.cpu_count() or 1
     cfg = SimConfig(width=WIDTH, height=HEIGHT, frame_count=1000, rng_seed=0)
-    n_frames = 24  # generated once, cycled (the state never repeats: it is recursive)
+    n_frames = min(24, max(8, args.steps + args.warmup + p.mz))  # generated once, cycled
     frames = generate_counter(cfg, frames=n_frames)
     with OraclePipeline(p, WIDTH, HEIGHT, threads=threads) as orc:
         k = 0
@@ -231,7 +246,7 @@ def run_ours(args):
         # NCCL's communicator-init log (ranks, transports) for the record
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist = init_dist(local)
     dev = torch.device("cuda", local)
     p = default_params()
     lib = _native.load()
@@ -433,8 +448,8 @@ def c4_strip_line(args, lib, dist, world, rank, local, dev):
         "metric": "pixel-frames/sec (4096x4096, strip-sharded)", "value": w * h * steps / (el / 1e3), "unit": UNIT,
         "n_gpus": world, "steps": steps, "ms_per_step": el / steps, "scaling": "strong",
         "config": {"workload": "C4: 4096x4096 frames, row strips + (My-1)-row halo exchanged per frame over "
-                               + ("NCCL" if dist else "nothing (one strip)"),
-                   "frame": [w, h], "strips": world, "strip_rows": rows, "halo_rows": pl.halo},
+                               + (dist.get_backend().upper() if dist else "nothing (one strip)"),
+                   "frame": [w, h], "strips": world, "strip_rows": rows, "halo_rows": p.my - 1 if world > 1 else 0},
         "gpu_launches": steps, "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                                             "frac": achieved / peak, "peak_kind": peak_kind, "kernel_ms": kern,
                                             "bytes_per_px_frame": bpp},
@@ -525,7 +540,7 @@ def run_config(args):
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist = init_dist(local)
     dev = torch.device("cuda", local)
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)

@@ -4,11 +4,12 @@ Pipeline's pre-device checks, against the reference's behaviour
 known answers (test_params.py, test_design.py, test_pipeline.py)."""
 
 import math
+import os
 
 import numpy as np
 import pytest
 
-from conftest import golden
+from conftest import ROOT, golden
 from paper_1408_3526_b200 import (
     ExecStrategy, FilterParams, ParamError, Pipeline, build_bank, default_params, dirichlet,
     kernel_to_freq, load_params, pick_gains, retained_bin_indices, sample_kernel, save_params,
@@ -198,3 +199,24 @@ def test_product_package_never_touches_the_oracle():
                 assert (node.module or "").split(".")[0] != "oracle", name
             elif isinstance(node, ast.Constant) and isinstance(node.value, str):
                 assert "libcw_oracle" not in node.value, name
+
+
+def test_reference_arm_line_on_cpu():
+    """bench.py --impl reference (the reference algorithm = the float64 oracle
+    on the host cores): same metric, workload and unit as the GPU arm, with
+    the cpu_baseline / e2e objects the contract asks for."""
+    import json
+    import subprocess
+    import sys
+
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "2",
+                          "--warmup", "3", "--ref-budget", "0.5"], capture_output=True, text=True, cwd=ROOT,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    import bench
+
+    assert d["impl"] == "reference" and d["metric"] == bench.METRIC and d["unit"] == bench.UNIT
+    assert d["config"]["workload"] == bench.WORKLOAD and d["config"]["frame"] == [640, 512]
+    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["value"] == d["value"] > 0
+    assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
