@@ -83,6 +83,11 @@ constexpr int RESTART = CW_RESTART;  // rows between direct y-SDFT restarts (bou
 // host) instead of a 32 KB retained-z+ stage in shared memory
 #define CW_PEF_L2 0
 #endif
+#ifndef CW_SBULK
+// updated observer state written into the staged packet in place and sent
+// to HBM by TMA bulk stores (one per kx column of a row) instead of STG
+#define CW_SBULK 0
+#endif
 #ifndef CW_TBULK
 // T^ write-back as one TMA bulk store of the smoothed T^ stage (issued after
 // barrier 2 by the issuing thread) instead of per-warp STG
@@ -691,6 +696,29 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                 if (!G::PEF_L2) sret[q * 32 + lane] = f2(v);
             };
             cf cz[MX][MZ];  // 4 x Hz(z+) per kx column
+            // state write-back: STG, or (SBULK) in place + bulk stores of pairs
+            // [j0, j1) of this warp's row once the warp has written them
+            constexpr bool SBULK = CW_SBULK && !G::PEF_L2;
+            auto put_state = [&](int j, float2 v) {
+                if (SBULK) sst[j * 32] = v;
+                else st_state(&stg[j * 32], v);
+            };
+            auto flush_state = [&](int j0, int j1) {
+                if (SBULK) {
+                    fence_proxy_async();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tma_store(stg - lane + j0 * 32, sst - lane + j0 * 32, (uint32_t)(j1 - j0) * 256);
+                        tma_store_commit();
+                    }
+                }
+            };
+            auto flush_wait = [&]() {  // the bulk stores have read the row: it may be overwritten
+                if (SBULK) {
+                    if (lane == 0) tma_store_wait_read();
+                    __syncwarp();
+                }
+            };
             if (CW_MEMONLY == 2) {  // diagnostic: the same traffic, state written back by one bulk store
                 if (threadIdx.x == ISSUER) {
                     tma_store(a.state + pix * G::NSP * 32, stage, G::SM_STAGE);
@@ -711,12 +739,12 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                     for (int kz = 1; kz <= KZ; kz++) sum = fmaf(2.f, zd[kz].r, sum);
                     const float e = fmaf(-t.inv_mz, sum, uv);
                     const float z0 = zd[0].r + e;
-                    st_state(&stg[0], make_float2(z0, 0.f));
+                    put_state(0, make_float2(z0, 0.f));
                     rput(0, cmk(z0, 0.f));
 #pragma unroll
                     for (int kz = 1; kz <= KZ; kz++) {
                         const cf zp = cmk(zd[kz].r + e, zd[kz].i);
-                        st_state(&stg[kz * 32], f2(cmulw(zp, t.w2[kz + KZ], t.wn2[kz + KZ])));
+                        put_state(kz, f2(cmulw(zp, t.w2[kz + KZ], t.wn2[kz + KZ])));
                         rput(kz, zp);
                     }
                 }
@@ -740,7 +768,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                     for (int kzi = 0; kzi < MZ; kzi++) {
                         zp[kzi] = cadd(z[kzi], e);
                         const cf zn = (kzi == KZ) ? zp[kzi] : cmulw(zp[kzi], t.w2[kzi], t.wn2[kzi]);
-                        st_state(&stg[(base + kzi) * 32], f2(zn));
+                        put_state(base + kzi, f2(zn));
                         if (kx <= BX) rput(base + kzi, zp[kzi]);
                     }
 #pragma unroll
@@ -748,11 +776,13 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                         cz[KX + kx][kzi] = hann4(zp[(kzi + MZ - 1) % MZ], zp[kzi], zp[(kzi + 1) % MZ]);
                 }
                 if (G::PROW0P & 1) rput(G::PROW0P, cmk(0.f, 0.f));  // pad pair (zero coefficient)
+                flush_state(0, G::ROW0P);
                 // kx < 0 by symmetry: C(kz, 0, -kx) = conj C(-kz, 0, kx)
 #pragma unroll
                 for (int kx = 1; kx <= KX; kx++)
 #pragma unroll
                     for (int kzi = 0; kzi < MZ; kzi++) cz[KX - kx][kzi] = cconj(cz[KX + kx][MZ - 1 - kzi]);
+                flush_wait();
                 if (a.ready) {
                     // Hx, compact row 0 in place: kx = 0 (kz = 0..KZ), kx = 1..KX (all kz)
 #pragma unroll
@@ -788,14 +818,16 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                     for (int kzi = 0; kzi < MZ; kzi++) {
                         zp[kzi] = cadd(z[kzi], e);
                         const cf zn = (kzi == KZ) ? zp[kzi] : cmulw(zp[kzi], t.w2[kzi], t.wn2[kzi]);
-                        st_state(&stg[(kxi * MZ + kzi) * 32], f2(zn));
+                        put_state(kxi * MZ + kzi, f2(zn));
                         if (r <= BY && kxb >= 0 && kxb < G::WX) rput(2 * rq + kxb * MZ + kzi, zp[kzi]);
                     }
 #pragma unroll
                     for (int kzi = 0; kzi < MZ; kzi++)
                         cz[kxi][kzi] = hann4(zp[(kzi + MZ - 1) % MZ], zp[kzi], zp[(kzi + 1) % MZ]);
+                    flush_state(kxi * MZ, (kxi + 1) * MZ);
                 }
                 if (r <= BY && (G::PROWNP & 1)) rput(2 * rq + G::PROWNP, cmk(0.f, 0.f));  // pad pair
+                flush_wait();
                 if (a.ready) {
                     // Hx (circular along kx), in place over this row's staged state
 #pragma unroll
@@ -1249,6 +1281,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
         u += ye - ys;
     }
     if (CW_TBULK && threadIdx.x == ISSUER) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    if (CW_SBULK && !G::PEF_L2 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 #ifdef CW_PHASE_TIMING
     if (blockIdx.x == 0 && (threadIdx.x & 31) == 0)
         for (int k = 0; k < 11; k++) cw_phase_clk[threadIdx.x >> 5][k] += clk_acc[k];
