@@ -56,7 +56,8 @@ def instances(dev: bool = False):
     import re
 
     if dev:
-        return [(4, 4, 2, 3, 3, 0), (4, 4, 2, 3, 3, 17)]
+        g = tuple(int(v) for v in os.environ.get("CW_DEV_GEO", "4,4,2,3,3").split(","))
+        return [g + (0,), g + (17,)]
     src = open(os.path.join(CSRC, "cw_inst.cuh")).read()
     geos = re.findall(r"CW_INSTANCES_GEO\(X,\s*(\d+),\s*(\d+),\s*(\d+),\s*(\d+),\s*(\d+)\)", src)
     return [tuple(int(v) for v in g) + (n,) for g in geos for n in (0, 9, 17, 33)]
@@ -73,6 +74,8 @@ def build(verbose: bool = False, out: str | None = None, dev: bool = False, extr
     base = [f for f in NVCC_FLAGS if f != "-shared"] + list(extra)
     if dev:
         base.append("-DCW_DEV_DEFAULT_ONLY")
+        geo = os.environ.get("CW_DEV_GEO", "4,4,2,3,3").split(",")
+        base += [f"-DCW_DEV_{k}={v}" for k, v in zip(("KX", "KY", "KZ", "BX", "BY"), geo)]
     if verbose:
         base.append("-Xptxas=-v")
     with tempfile.TemporaryDirectory(prefix="cw_build_") as tmp:

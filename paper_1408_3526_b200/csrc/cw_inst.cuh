@@ -36,8 +36,17 @@ static void phase_clocks_read(unsigned long long *dst)  // [8][16] + CTA spans [
 
 // (KX, KY, KZ, BX, BY, NL): the default geometry and the SURVEY §8d C5 sweep;
 // NL = 9 / 17 / 33 are the fully unrolled symmetric-grid contractions.
-#ifdef CW_DEV_DEFAULT_ONLY  // dev builds (tools/dev_build.sh)
-#define CW_INSTANCES(X) X(4, 4, 2, 3, 3, 0) X(4, 4, 2, 3, 3, 17)
+#ifdef CW_DEV_DEFAULT_ONLY  // dev builds (tools/dev_build.sh; CW_DEV_GEO picks the geometry)
+#ifndef CW_DEV_KX  // -DCW_DEV_KX=.. -DCW_DEV_KY=.. (nvcc splits a comma list)
+#define CW_DEV_KX 4
+#define CW_DEV_KY 4
+#define CW_DEV_KZ 2
+#define CW_DEV_BX 3
+#define CW_DEV_BY 3
+#endif
+#define CW_DEV_X(X, a, b, c, d, e) X(a, b, c, d, e, 0) X(a, b, c, d, e, 17)
+#define CW_DEV_X2(X, a, b, c, d, e) CW_DEV_X(X, a, b, c, d, e)
+#define CW_INSTANCES(X) CW_DEV_X2(X, CW_DEV_KX, CW_DEV_KY, CW_DEV_KZ, CW_DEV_BX, CW_DEV_BY)
 #else
 #define CW_INSTANCES_GEO(X, a, b, c, d, e) X(a, b, c, d, e, 0) X(a, b, c, d, e, 9) X(a, b, c, d, e, 17) X(a, b, c, d, e, 33)
 #define CW_INSTANCES(X)                   \
