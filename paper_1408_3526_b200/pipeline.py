@@ -285,6 +285,13 @@ class Pipeline:
     def frames_seen(self) -> int:
         return int(_native.load().cw_frames_seen(self._h))
 
+    @property
+    def kernel_kind(self) -> str:
+        """Which device path runs these parameters: "compiled" (a fused
+        instance in the library), "jit" (the fused kernel compiled at run
+        time for this geometry) or "runtime-geometry"."""
+        return ("compiled", "jit", "runtime-geometry")[int(_native.load().cw_kernel_kind(self._h))]
+
     def set_strategy(self, strategy: ExecStrategy | str) -> None:
         """Accepted for compatibility; outputs are unaffected."""
         self._strategy = ExecStrategy.parse(strategy) if isinstance(strategy, str) else strategy

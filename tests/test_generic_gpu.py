@@ -57,6 +57,7 @@ def _run_kind(params, frames, **kw):
         outs = [o for o in map(pipe.process_frame, frames) if o is not None]
         kind = int(_native.load().cw_kernel_kind(pipe._h))
         assert bool(_native.load().cw_is_generic(pipe._h)) == (kind == 2)
+        assert pipe.kernel_kind == ("compiled", "jit", "runtime-geometry")[kind]
     return outs, kind
 
 
