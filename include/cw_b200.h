@@ -125,6 +125,27 @@ int cw_submit_device(cw_handle *h, const float *frame_dev, float *residual, floa
                      int64_t *ticket, void *producer);
 
 /*
+ * cw_submit for a frame that is already complete in device memory and stays
+ * unchanged until cw_wait(ticket) returns (resident inputs, e.g. a frame
+ * buffer filled before the stream starts).  No producer stream is joined
+ * and no copy is enqueued: the frame kernel reads `frame_dev` and fills its
+ * ring slot itself, and consecutive frame kernels are chained (programmatic
+ * dependent launch; each CTA waits only for its own units of the previous
+ * frame), so a frame's kernel starts in the SM slots the
+ * previous frame's early CTAs free.  Host output buffers may be NULL (the
+ * results stay on the device: cw_device_outputs after cw_wait).  Results are
+ * bit-identical to cw_push_device's with the static work split.
+ * (Not in the reference: its frames are host arrays, pipeline.py:201.)
+ */
+int cw_submit_resident(cw_handle *h, const float *frame_dev, float *residual, float *prediction, uint8_t *vidx,
+                       int64_t *ticket);
+
+/* Orders `stream` (a cudaStream_t) after every frame kernel submitted so far
+ * (device-side join, e.g. to consume cw_device_outputs on the caller's
+ * stream or to time a run of cw_submit_resident calls with events). */
+int cw_join(cw_handle *h, void *stream);
+
+/*
  * cw_submit for a frame in a sequence-file sample format (replaces the host
  * decode of read_sequence, seqio.py:172-204; the payloads of seqio.py:1-8):
  *   CW_FMT_F32LE: little-endian float32 (frames.f32), scale/offset ignored;

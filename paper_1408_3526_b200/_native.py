@@ -36,7 +36,7 @@ EXPORTS = (
     "cw_kernel_time", "cw_copy_to_host", "cw_submit", "cw_submit_raw", "cw_wait", "cw_set_detection", "cw_detections",
     "cw_set_backend", "cw_snapshot_size", "cw_snapshot", "cw_restore",
     "cw_scene_generate", "cw_scene_last_error", "cw_index_bytes", "cw_is_generic",
-    "cw_submit_device", "cw_kernel_kind", "cw_jit_prebuild",
+    "cw_submit_device", "cw_submit_resident", "cw_join", "cw_kernel_kind", "cw_jit_prebuild",
 )
 
 
@@ -57,7 +57,7 @@ def instances(dev: bool = False):
 
     if dev:
         g = tuple(int(v) for v in os.environ.get("CW_DEV_GEO", "4,4,2,3,3").split(","))
-        return [g + (0,), g + (17,)]
+        return [g + (0,), g + (17,), g + (33,)]
     src = open(os.path.join(CSRC, "cw_inst.cuh")).read()
     geos = re.findall(r"CW_INSTANCES_GEO\(X,\s*(\d+),\s*(\d+),\s*(\d+),\s*(\d+),\s*(\d+)\)", src)
     return [tuple(int(v) for v in g) + (n,) for g in geos for n in (0, 9, 17, 33)]
@@ -206,6 +206,8 @@ def load():
         "cw_submit_raw": (ctypes.c_int, [vp, vp, i32, ctypes.c_double, ctypes.c_double, vp, vp, vp, P(i64)]),
         "cw_wait": (ctypes.c_int, [vp, i64, P(i32), P(i64)]),
         "cw_submit_device": (ctypes.c_int, [vp, vp, vp, vp, vp, P(i64), vp]),
+        "cw_submit_resident": (ctypes.c_int, [vp, vp, vp, vp, vp, P(i64)]),
+        "cw_join": (ctypes.c_int, [vp, vp]),
         "cw_set_detection": (ctypes.c_int, [vp, ctypes.c_float, i32]),
         "cw_set_backend": (ctypes.c_int, [vp, i32]),
         "cw_snapshot_size": (ctypes.c_int, [vp, P(ctypes.c_size_t)]),

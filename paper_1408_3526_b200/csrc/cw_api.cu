@@ -14,6 +14,7 @@
 #ifdef _OPENMP
 #include <omp.h>
 #endif
+#include <cuda.h>  // CUstream / CUdeviceptr types of the stream memory operation entry point
 #include <nvtx3/nvToolsExt.h>  // header-only NVTX ranges (visible in nsys / ncu --nvtx)
 
 #include <algorithm>
@@ -104,6 +105,17 @@ struct cw_handle {
     unsigned char *d_rank = nullptr;  // compact instances: rank u16 [nl], then (ix, iy) u8 pairs [nl]
     double dyn_static = 0.92;  // measured on C3 (tools/ab_kernel.py): 0.92 / 2 rows, ~1% faster than all-static
     int dyn_chunk = 2;
+    // frame chaining (FrameArgs::done): per-CTA completion flags of the fused
+    // kernel; with `chain` the split is static and every fused launch is a
+    // programmatic dependent launch, so consecutive frames overlap
+    unsigned int *d_done = nullptr;
+    unsigned int seq = 0;
+    bool chain = true;         // CW_CHAIN=0 turns it off
+    bool last_static = false;  // the last fused launch used the static split
+    // chained cw_submit: cuStreamWriteValue32 (driver entry point; null: not
+    // available -> event waits) and its flags [0] upload, [1] download
+    CUresult (*write_value)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
+    unsigned int *d_flags = nullptr;
     int nslots = 0;  // frame ring slots: max(mhat_z + 2, Mz + 1) (async upload spare; naive window)
     bool naive = false;  // spectrum backend: false = recursive (observer), true = naive window DFT
     int naive_grid = 0;
@@ -111,8 +123,10 @@ struct cw_handle {
     cudaStream_t up = nullptr, down = nullptr;
     static constexpr int NEV = 8;
     cudaEvent_t ev_up[NEV] = {}, ev_k[NEV] = {}, ev_down[NEV] = {};
+    cudaEvent_t ev_join = nullptr;  // cw_join
     int ready_of[NEV] = {};
     long long fidx_of[NEV] = {};
+    bool dl_flagged[NEV] = {};  // chained cw_submit: the frame's download is followed by a flag write
     // detection epilogue: 2 device sets (double-buffered like the outputs),
     // NEV pinned host mirrors (one per outstanding frame)
     float det_tau = 0.f;
@@ -133,6 +147,10 @@ struct cw_handle {
     size_t ev_used = 0;
     std::string err;
 };
+
+// frame chaining applies to the fused kernel with the recursive backend;
+// the in-kernel ring fill needs the delayed frame two launches back or more
+static bool chained(const cw_handle *h) { return h->chain && !h->generic && !h->naive && h->mhz >= 2; }
 
 static int fail(cw_handle *h, int code, const std::string &msg)
 {
@@ -672,14 +690,30 @@ int cw_create(const cw_params *p, int32_t width, int32_t height, int32_t device,
             cudaEventCreateWithFlags(&h->ev_k[i], cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&h->ev_down[i], cudaEventDisableTiming) != cudaSuccess)
             return cleanup_fail(CW_ERR_CUDA, "cudaEventCreate failed");
+    if (cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess)
+        return cleanup_fail(CW_ERR_CUDA, "cudaEventCreate failed");
     if (!generic)
         cudaMemcpyAsync(h->d_coef, coef.data(), coef.size() * 4, cudaMemcpyHostToDevice, h->own);
     if (const char *e = std::getenv("CW_DYN_STATIC"))  // tuning knobs (tools/ab_kernel.py)
         h->dyn_static = std::atof(e);
     if (const char *e = std::getenv("CW_DYN_CHUNK"))
         h->dyn_chunk = std::max(1, std::atoi(e));
-    if (cudaMalloc(&h->d_work, 2 * sizeof(unsigned int)) != cudaSuccess)
+    if (const char *e = std::getenv("CW_CHAIN"))
+        h->chain = std::atoi(e) != 0;
+    if (cudaMalloc(&h->d_work, 2 * sizeof(unsigned int)) != cudaSuccess ||
+        cudaMalloc(&h->d_done, sizeof(unsigned int) * std::max(1, h->grid)) != cudaSuccess)
         return cleanup_fail(CW_ERR_NOMEM, "device allocation failed");
+    cudaMemsetAsync(h->d_done, 0, sizeof(unsigned int) * std::max(1, h->grid), h->own);
+    {
+        void *fp = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &fp, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess && fp && cudaMalloc(&h->d_flags, 2 * sizeof(unsigned int)) == cudaSuccess) {
+            h->write_value = reinterpret_cast<decltype(h->write_value)>(fp);
+            cudaMemsetAsync(h->d_flags, 0, 2 * sizeof(unsigned int), h->own);
+        }
+        cudaGetLastError();
+    }
     if (!generic && fn.compact) {  // the rank tables the compact instance reads from global memory
         const int nl = h->nlx * h->nly;
         std::vector<unsigned char> rk((size_t)nl * 4);
@@ -716,6 +750,8 @@ void cw_destroy(cw_handle *h)
     cudaFree(h->d_vidx);
     cudaFree(h->d_gtab);
     cudaFree(h->d_work);
+    cudaFree(h->d_done);
+    cudaFree(h->d_flags);
     cudaFree(h->d_rank);
     cudaFree(h->d_xf);
     cudaFree(h->d_det);
@@ -733,6 +769,9 @@ void cw_destroy(cw_handle *h)
         if (h->ev_up[i]) cudaEventDestroy(h->ev_up[i]);
         if (h->ev_k[i]) cudaEventDestroy(h->ev_k[i]);
         if (h->ev_down[i]) cudaEventDestroy(h->ev_down[i]);
+    }
+    if (h->ev_join) {
+        cudaEventDestroy(h->ev_join);
     }
     if (h->up) {
         cudaStreamSynchronize(h->up);
@@ -814,9 +853,21 @@ struct NvtxRange {
 // Outputs go to the handle's double-buffered device set unless res_o /
 // pred_o / vidx_o (device-addressable pointers, e.g. mapped host memory)
 // override them.
+struct FlagWants {
+    unsigned int up_want, down_want;
+};
+
 static int run_frame(cw_handle *h, cudaStream_t s, int32_t *ready, int64_t *frame_index, float *res_o = nullptr,
-                     float *pred_o = nullptr, uint8_t *vidx_o = nullptr)
+                     float *pred_o = nullptr, uint8_t *vidx_o = nullptr, const float *frame_src = nullptr,
+                     bool chain = false, const FlagWants *flags = nullptr)
 {
+    // chain: static split, and a programmatic dependent launch when the
+    // previous fused launch was static too (done[] then names the same
+    // units per CTA); otherwise a plain launch (full stream order), which
+    // may use the dynamic tail
+    chain = chain && chained(h);
+    const bool pdl = chain && h->last_static;
+    h->dl_flagged[h->frames_seen % cw_handle::NEV] = false;  // set again by a flagged cw_submit
     NvtxRange nvtx("cw_frame");
     const size_t HW = (size_t)h->W * h->H;
     const long long n = h->frames_seen;
@@ -846,7 +897,7 @@ static int run_frame(cw_handle *h, cudaStream_t s, int32_t *ready, int64_t *fram
         const long long units = (long long)h->NXB * (h->H - h->halo);
         const long long su = (long long)(h->dyn_static * (double)units);
         // dynamic chunks pay a run restart each: only for long per-CTA runs
-        const bool dyn = h->dyn_static < 1.0 && su < units && units >= 20LL * h->grid;
+        const bool dyn = !chain && h->dyn_static < 1.0 && su < units && units >= 20LL * h->grid;
         a.work = dyn ? h->d_work : nullptr;
         a.parity = (int)(n & 1);
         a.static_units = su < 0 ? 0 : su;
@@ -855,6 +906,23 @@ static int run_frame(cw_handle *h, cudaStream_t s, int32_t *ready, int64_t *fram
     a.rank_g = reinterpret_cast<const uint16_t *>(h->d_rank);
     a.rxy_g = h->d_rank ? h->d_rank + (size_t)h->nlx * h->nly * 2 : nullptr;
     a.det = nullptr;
+    a.done = h->d_done;
+    a.seq = ++h->seq;
+    a.ring_dst = nullptr;
+    a.up_flag = a.down_flag = nullptr;
+    a.up_want = a.down_want = 0;
+    if (flags) {
+        a.up_flag = h->d_flags;
+        a.up_want = flags->up_want;
+        if (flags->down_want) {
+            a.down_flag = h->d_flags + 1;
+            a.down_want = flags->down_want;
+        }
+    }
+    if (frame_src) {  // chained push: the kernel reads the caller's frame and fills the slot
+        a.ring_dst = const_cast<float *>(a.frame);
+        a.frame = frame_src;
+    }
     a.det_tau = h->det_tau;
     a.det_cap = h->det_cap;
     if (h->det_on && rd) {
@@ -937,13 +1005,29 @@ static int run_frame(cw_handle *h, cudaStream_t s, int32_t *ready, int64_t *fram
         CW_CUDA(h, cudaGetLastError());
     }
     if (!h->generic) {
-        if (h->fn.launch) {
+        if (pdl) {
+            // programmatic dependent launch: may start while the previous
+            // frame's kernel drains; the kernel orders itself per CTA (done[])
+            void *args[] = {&a, &h->tab};
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(h->grid);
+            cfg.blockDim = dim3(h->fn.threads);
+            cfg.dynamicSmemBytes = h->fn.smem;
+            cfg.stream = s;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            CW_CUDA(h, cudaLaunchKernelExC(&cfg, h->fn.kernel, args));
+        } else if (h->fn.launch) {
             h->fn.launch(a, h->tab, h->grid, s);
         } else {  // run-time compiled instance
             void *args[] = {&a, &h->tab};
             CW_CUDA(h, cudaLaunchKernel(h->fn.kernel, dim3(h->grid), dim3(h->fn.threads), args, h->fn.smem, s));
         }
         CW_CUDA(h, cudaGetLastError());
+        h->last_static = a.work == nullptr;
     }
     if (h->timing)
         CW_CUDA(h, cudaEventRecord(e1, s));
@@ -1210,6 +1294,12 @@ static int submit_impl(cw_handle *h, const void *samples, int format, double sca
     if (n >= 2)
         CW_CUDA(h, cudaStreamWaitEvent(h->up, h->ev_k[(n - 2) % cw_handle::NEV], 0));
     float *slot = h->d_frames + (size_t)(n % h->nslots) * HW;
+    // chained: the kernel's stream carries no cross-stream wait (it would
+    // serialise consecutive frame kernels); the upload and the download of
+    // frame n - 2 (this output set) post flags the kernel waits on instead.
+    // Only copy-engine work may feed a flag the kernel spins on: the PGM16
+    // decode kernel needs SM slots the spinning CTAs could hold.
+    const bool flagged = chained(h) && h->write_value && format != CW_FMT_PGM16;
     if (format == CW_FMT_PGM16) {
         if (!h->d_raw) {
             CW_CUDA(h, cudaMalloc(&h->d_raw, HW * 2 + 16));
@@ -1224,13 +1314,24 @@ static int submit_impl(cw_handle *h, const void *samples, int format, double sca
         CW_CUDA(h, cudaMemcpyAsync(slot, frame, HW * 4, cudaMemcpyHostToDevice, h->up));
     }
     CW_CUDA(h, cudaEventRecord(h->ev_up[e], h->up));
-    CW_CUDA(h, cudaStreamWaitEvent(h->own, h->ev_up[e], 0));
-    if (n >= 2)
-        CW_CUDA(h, cudaStreamWaitEvent(h->own, h->ev_down[(n - 2) % cw_handle::NEV], 0));
+    FlagWants fw{};
+    if (flagged) {
+        const unsigned int tag = (unsigned int)(n + 1);
+        if (h->write_value(reinterpret_cast<CUstream>(h->up), reinterpret_cast<CUdeviceptr>(h->d_flags), tag, 0) !=
+            CUDA_SUCCESS)
+            return fail(h, CW_ERR_CUDA, "cuStreamWriteValue32 failed");
+        fw.up_want = tag;
+        // frame n - 2 wrote this output set; its download posted n - 1
+        fw.down_want = (n >= 2 && h->dl_flagged[(n - 2) % cw_handle::NEV]) ? (unsigned int)(n - 1) : 0u;
+    } else {
+        CW_CUDA(h, cudaStreamWaitEvent(h->own, h->ev_up[e], 0));
+        if (n >= 2)
+            CW_CUDA(h, cudaStreamWaitEvent(h->own, h->ev_down[(n - 2) % cw_handle::NEV], 0));
+    }
     int32_t rd = 0;
     int64_t fi = -1;
     const size_t set = (size_t)(n & 1);
-    int rc = run_frame(h, h->own, &rd, &fi);
+    int rc = run_frame(h, h->own, &rd, &fi, nullptr, nullptr, nullptr, nullptr, true, flagged ? &fw : nullptr);
     if (rc != CW_OK)
         return rc;
     CW_CUDA(h, cudaEventRecord(h->ev_k[e], h->own));
@@ -1242,6 +1343,12 @@ static int submit_impl(cw_handle *h, const void *samples, int format, double sca
             CW_CUDA(h, cudaMemcpyAsync(prediction, h->d_pred + set * HW, HW * 4, cudaMemcpyDeviceToHost, h->down));
         if (vidx)
             CW_CUDA(h, cudaMemcpyAsync(vidx, h->d_vidx + set * HW * 2 * h->idx_bytes, HW * 2 * h->idx_bytes, cudaMemcpyDeviceToHost, h->down));
+    }
+    if (flagged) {
+        if (h->write_value(reinterpret_cast<CUstream>(h->down), reinterpret_cast<CUdeviceptr>(h->d_flags + 1),
+                           (unsigned int)(n + 1), 0) != CUDA_SUCCESS)
+            return fail(h, CW_ERR_CUDA, "cuStreamWriteValue32 failed");
+        h->dl_flagged[e] = true;
     }
     CW_CUDA(h, cudaEventRecord(h->ev_down[e], h->down));
     h->ready_of[e] = rd;
@@ -1256,8 +1363,23 @@ static int submit_impl(cw_handle *h, const void *samples, int format, double sca
 // stream is then ordered after that copy (the caller may overwrite its
 // buffer with work enqueued later on `producer`); kernel and result download
 // overlap the next frames exactly as cw_submit's.
+static int submit_device_impl(cw_handle *h, const float *frame_dev, float *residual, float *prediction,
+                              uint8_t *vidx, int64_t *ticket, void *producer, bool resident_frame);
+
 int cw_submit_device(cw_handle *h, const float *frame_dev, float *residual, float *prediction, uint8_t *vidx,
                      int64_t *ticket, void *producer)
+{
+    return submit_device_impl(h, frame_dev, residual, prediction, vidx, ticket, producer, false);
+}
+
+int cw_submit_resident(cw_handle *h, const float *frame_dev, float *residual, float *prediction, uint8_t *vidx,
+                       int64_t *ticket)
+{
+    return submit_device_impl(h, frame_dev, residual, prediction, vidx, ticket, nullptr, true);
+}
+
+static int submit_device_impl(cw_handle *h, const float *frame_dev, float *residual, float *prediction,
+                              uint8_t *vidx, int64_t *ticket, void *producer, bool resident_frame)
 {
     NvtxRange nvtx("cw_submit_device");
     DeviceGuard dg(h);
@@ -1268,20 +1390,31 @@ int cw_submit_device(cw_handle *h, const float *frame_dev, float *residual, floa
     const int e = (int)(n % cw_handle::NEV);
     if (n >= cw_handle::NEV)  // ticket n - NEV must have been collected
         CW_CUDA(h, cudaEventSynchronize(h->ev_down[e]));
-    cudaStream_t ps = reinterpret_cast<cudaStream_t>(producer);
-    CW_CUDA(h, cudaEventRecord(h->ev_up[e], ps));
-    CW_CUDA(h, cudaStreamWaitEvent(h->own, h->ev_up[e], 0));
     float *slot = h->d_frames + (size_t)(n % h->nslots) * HW;
-    if (slot != frame_dev)
-        CW_CUDA(h, cudaMemcpyAsync(slot, frame_dev, HW * 4, cudaMemcpyDeviceToDevice, h->own));
-    CW_CUDA(h, cudaEventRecord(h->ev_up[e], h->own));
-    CW_CUDA(h, cudaStreamWaitEvent(ps, h->ev_up[e], 0));
-    if (n >= 2)
+    // cw_submit_resident: the frame is complete in device memory and stays
+    // unchanged until this ticket is collected -- the kernel reads it and
+    // fills its ring slot itself, so consecutive frame kernels overlap
+    // (chained); without chaining it is copied as cw_submit_device's
+    const bool resident = resident_frame && chained(h) && slot != frame_dev;
+    if (!resident) {
+        cudaStream_t ps = reinterpret_cast<cudaStream_t>(producer);
+        CW_CUDA(h, cudaEventRecord(h->ev_up[e], ps));
+        CW_CUDA(h, cudaStreamWaitEvent(h->own, h->ev_up[e], 0));
+        if (slot != frame_dev)
+            CW_CUDA(h, cudaMemcpyAsync(slot, frame_dev, HW * 4, cudaMemcpyDeviceToDevice, h->own));
+        CW_CUDA(h, cudaEventRecord(h->ev_up[e], h->own));
+        CW_CUDA(h, cudaStreamWaitEvent(ps, h->ev_up[e], 0));
+    }
+    // the output set of frame n - 2 is downloaded before kernel n rewrites
+    // it; with no host outputs there is no download, and no wait: a pending
+    // cross-stream wait between two frame kernels would serialise them
+    // (measured: it cancels the programmatic launch)
+    if (n >= 2 && (residual || prediction || vidx || !resident))
         CW_CUDA(h, cudaStreamWaitEvent(h->own, h->ev_down[(n - 2) % cw_handle::NEV], 0));
     int32_t rd = 0;
     int64_t fi = -1;
     const size_t set = (size_t)(n & 1);
-    int rc = run_frame(h, h->own, &rd, &fi);
+    int rc = run_frame(h, h->own, &rd, &fi, nullptr, nullptr, nullptr, resident ? frame_dev : nullptr, resident);
     if (rc != CW_OK)
         return rc;
     CW_CUDA(h, cudaEventRecord(h->ev_k[e], h->own));
@@ -1299,6 +1432,16 @@ int cw_submit_device(cw_handle *h, const float *frame_dev, float *residual, floa
     h->ready_of[e] = rd;
     h->fidx_of[e] = fi;
     *ticket = n;
+    return CW_OK;
+}
+
+int cw_join(cw_handle *h, void *stream)
+{
+    DeviceGuard dg(h);
+    if (!h)
+        return CW_ERR_VALUE;
+    CW_CUDA(h, cudaEventRecord(h->ev_join, h->own));
+    CW_CUDA(h, cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(stream), h->ev_join, 0));
     return CW_OK;
 }
 
@@ -1456,6 +1599,11 @@ int cw_restore(cw_handle *h, const void *src, size_t bytes)
     CW_CUDA(h, cudaMemcpy(h->d_frames, p, hd.frames_bytes, cudaMemcpyHostToDevice));
     h->frames_seen = hd.frames_seen;
     h->have_that = hd.have_that != 0;
+    // the submit flags are tagged with frame numbers: restart them
+    if (h->d_flags)
+        CW_CUDA(h, cudaMemset(h->d_flags, 0, 2 * sizeof(unsigned int)));
+    for (bool &f : h->dl_flagged)
+        f = false;
     return CW_OK;
 }
 

@@ -96,6 +96,15 @@ constexpr int RESTART = CW_RESTART;  // rows between direct y-SDFT restarts (bou
 #ifndef CW_FENCE_ALL
 #define CW_FENCE_ALL 1  // every thread orders its generic stage reads before the next TMA write
 #endif
+#ifndef CW_JQ_WIDE
+#define CW_JQ_WIDE 1  // lag column pairs per contraction group for grids of more than 17 lags (2: 1.73 vs 1.27 ms, C5 lag 1/8)
+#endif
+#ifndef CW_PQ_UNROLL_WIDE
+#define CW_PQ_UNROLL_WIDE 16  // unroll of the stage-2 lag loop for grids of more than 17 lags
+#endif
+#ifndef CW_ROLL_WIDE
+#define CW_ROLL_WIDE 1  // the group loop of grids of more than 17 lags is not unrolled (instruction cache)
+#endif
 
 struct alignas(16) LagRec {
     float gain, pad;
@@ -169,6 +178,27 @@ struct FrameArgs {
     unsigned char *det;
     float det_tau;  // |res| >= det_tau is a detection (<= 0: list off)
     int det_cap;
+    // frame chaining: CTA i of a launch works on exactly the (column block,
+    // row) units CTA i of the previous launch worked on (static split, same
+    // grid), so it needs only that CTA's packets: it waits for
+    // done[i] >= seq - 1 before its first state / T^ / output access and
+    // publishes done[i] = seq when it is through.  With programmatic
+    // dependent launch (cw_api.cu) the next frame's CTAs start in the SM
+    // slots this frame's early finishers free, instead of after its last CTA.
+    unsigned int *done;  // [grid] (nullable: no chaining)
+    unsigned int seq;
+    // chained pushes of device frames: `frame` is the caller's buffer and the
+    // kernel copies it into this ring slot itself (a share per CTA, once
+    // every CTA of launch seq - 2 is through: the slot's previous frame and
+    // the delayed frame are then no longer / already written), so no copy
+    // sits between consecutive frame kernels (nullable)
+    float *ring_dst;
+    // chained cw_submit: the frame upload and the previous download of this
+    // output set signal completion by stream memory writes (cw_api.cu)
+    // instead of events the kernel's stream would wait on; the kernel waits
+    // for up_flag >= up_want and down_flag >= down_want (nullable)
+    const unsigned int *up_flag, *down_flag;
+    unsigned int up_want, down_want;
 };
 
 // Fused "final threshold" and the ground-truth-free metrics of
@@ -401,6 +431,25 @@ __device__ __forceinline__ void tma_load(void *dst, const void *src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_addr(bar))
         : "memory");
 }
+// frame chaining (FrameArgs::done): acquire-wait on this CTA's flag, bounded
+// (a lost flag traps instead of hanging the GPU)
+__device__ __forceinline__ void chain_wait(const unsigned int *flag, unsigned int want)
+{
+    unsigned int v, ns = 32;
+    for (long long it = 0;; it++) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+        if ((int)(v - want) >= 0) break;
+        if (it > (1ll << 24)) asm volatile("trap;");
+        __nanosleep(ns);
+        ns = ns < 256 ? 2 * ns : 256;
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // later TMA reads see the acquired writes
+}
+__device__ __forceinline__ void chain_publish(unsigned int *flag, unsigned int v)
+{
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase)
 {
     uint32_t ok = 0;
@@ -533,6 +582,20 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
         fence_mbar_init();
     }
     if (a.work && blockIdx.x == 0 && threadIdx.x == 0) a.work[a.parity ^ 1] = 0u;
+    // the next frame's launch may start now (it waits on done[] per CTA)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if ((a.up_flag || a.down_flag) && threadIdx.x == G::NTHREADS - 32) {
+        if (a.up_flag) chain_wait(a.up_flag, a.up_want);
+        if (a.down_flag) chain_wait(a.down_flag, a.down_want);
+    }
+    if (a.ring_dst) {
+        if (r == KY)
+            for (int j = lane; j < (int)gridDim.x; j += 32) chain_wait(a.done + j, a.seq - 2u);
+        __syncthreads();
+        const size_t n = (size_t)W * H, b0 = n * blockIdx.x / gridDim.x, b1 = n * (blockIdx.x + 1) / gridDim.x;
+        for (size_t i = b0 + threadIdx.x; i < b1; i += G::NTHREADS) a.ring_dst[i] = __ldg(a.frame + i);
+    }
+    if (a.done && threadIdx.x == G::NTHREADS - 32) chain_wait(a.done + blockIdx.x, a.seq - 1u);  // the TMA issuer
     __syncthreads();
     uint32_t phase = 0, phase_t = 0;
 
@@ -1121,12 +1184,13 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                             co[c] = 0.f;
                             cpi[c] = 0;
                         }
-#pragma unroll
+                        constexpr int PQU = NL > 17 ? CW_PQ_UNROLL_WIDE : (C0 > 0 ? C0 : 1);
+#pragma unroll PQU
                         for (int pq = 1; pq <= C0; pq++) {
                             const LagRec &L2 = t.s2v[C0 + pq];
 #pragma unroll
                             for (int c = 0; c < 2 * JQ; c++) {
-                                // (e, o) = (g b0 + sum c Re B, sum s Im B); scores e -+ o
+                                    // (e, o) = (g b0 + sum c Re B, sum s Im B); scores e -+ o
                                 cf eo = cmk(L2.gain * b0[c], 0.f);
 #pragma unroll
                                 for (int k = 1; k <= KY; k++) eo = cfma2(c2(L2.cs[k - 1]), bq[c][k], eo);
@@ -1146,12 +1210,26 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                             if (better(cv[c], rk, best, brk)) { best = cv[c]; brk = rk; }
                         }
                     };
-                    constexpr int NG2 = QPW / 2;
+                    {
+                        constexpr int JW = NL > 17 ? CW_JQ_WIDE : 2;
+                        constexpr int NG2 = QPW / JW;
+                        // (a group's first pair q0 is on the grid; JW = 1: the last
+                        // round of q can run past it and is skipped)
+                        if (NL > 17 && CW_ROLL_WIDE) {
+#pragma unroll 1
+                            for (int i = 0; i < NG2; i++)
+                                if (JW == 2 || r + i * NR <= C0)
+                                    group(std::integral_constant<int, JW>{}, r + JW * i * NR);
+                        } else {
 #pragma unroll
-                    for (int i = 0; i < NG2; i++) group(std::integral_constant<int, 2>{}, r + 2 * i * NR);
-                    if (QPW & 1) {
-                        const int q0 = r + (QPW - 1) * NR;
-                        if (q0 <= C0) group(std::integral_constant<int, 1>{}, q0);
+                            for (int i = 0; i < NG2; i++)
+                                if (JW == 2 || r + i * NR <= C0)
+                                    group(std::integral_constant<int, JW>{}, r + JW * i * NR);
+                        }
+                        if (JW == 2 && (QPW & 1)) {
+                            const int q0 = r + (QPW - 1) * NR;
+                            if (q0 <= C0) group(std::integral_constant<int, 1>{}, q0);
+                        }
                     }
                 } else {
                     for (int lx = r; lx < nlx; lx += NR) {
@@ -1282,6 +1360,11 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
     }
     if (CW_TBULK && threadIdx.x == ISSUER) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     if (CW_SBULK && !G::PEF_L2 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    if (a.done) {  // every thread's state / T^ / output stores before the flag
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) chain_publish(a.done + blockIdx.x, a.seq);
+    }
 #ifdef CW_PHASE_TIMING
     if (blockIdx.x == 0 && (threadIdx.x & 31) == 0)
         for (int k = 0; k < 11; k++) cw_phase_clk[threadIdx.x >> 5][k] += clk_acc[k];

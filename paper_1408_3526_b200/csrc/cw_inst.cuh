@@ -44,7 +44,7 @@ static void phase_clocks_read(unsigned long long *dst)  // [8][16] + CTA spans [
 #define CW_DEV_BX 3
 #define CW_DEV_BY 3
 #endif
-#define CW_DEV_X(X, a, b, c, d, e) X(a, b, c, d, e, 0) X(a, b, c, d, e, 17)
+#define CW_DEV_X(X, a, b, c, d, e) X(a, b, c, d, e, 0) X(a, b, c, d, e, 17) X(a, b, c, d, e, 33)
 #define CW_DEV_X2(X, a, b, c, d, e) CW_DEV_X(X, a, b, c, d, e)
 #define CW_INSTANCES(X) CW_DEV_X2(X, CW_DEV_KX, CW_DEV_KY, CW_DEV_KZ, CW_DEV_BX, CW_DEV_BY)
 #else

@@ -1,0 +1,161 @@
+"""Frame chaining: consecutive frame kernels overlap
+(programmatic dependent launch, per-CTA completion flags, in-kernel ring
+fill for resident frames, stream-memory-write flags for cw_submit).  The
+chained entry points must give bit-identical results to plain, fully
+serialised launches with the same (static) work split, across frame sizes
+whose CTA runs are short (C2-like) and long, mixed entry points, and a
+snapshot restore in the middle of a chained stream."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _frames(t, h, w, seed=0):
+    rng = np.random.default_rng(seed)
+    xs, ys = np.arange(w)[None, :], np.arange(h)[:, None]
+    return np.stack([
+        10.0 + 0.3 * np.cos(2 * np.pi * ((xs - 1.25 * n) / 9.0 + (ys - 0.5 * n) / 7.0))
+        + 0.05 * rng.standard_normal((h, w)) for n in range(t)
+    ]).astype(np.float32)
+
+
+def _dev_outputs(lib, pipe, native):
+    w, h = pipe.width, pipe.height
+    ptrs = [ctypes.c_void_p() for _ in range(3)]
+    native.check(lib.cw_device_outputs(pipe._h, *[ctypes.byref(q) for q in ptrs]), pipe._h)
+    out = []
+    for q, nb in zip(ptrs, (w * h * 4, w * h * 4, w * h * 2 * pipe._idx_bytes)):
+        buf = np.empty(nb, np.uint8)
+        native.check(lib.cw_copy_to_host(pipe._h, buf.ctypes.data, q, nb), pipe._h)
+        out.append(buf)
+    return out
+
+
+def _run(params, frames, modes, monkeypatch, chain=True):
+    """Push `frames` through one pipeline, frame k by modes[k % len(modes)]
+    ("push": cw_push_device on torch's stream, "resident": cw_submit_resident,
+    "submit": cw_submit with pinned host frames and outputs); returns the
+    per-frame residuals that are observable (host outputs of "submit",
+    device outputs after "push") and the final snapshot + device outputs."""
+    import torch
+
+    from paper_1408_3526_b200 import Pipeline, _native
+
+    monkeypatch.setenv("CW_CHAIN", "1" if chain else "0")
+    monkeypatch.setenv("CW_DYN_STATIC", "1")  # the split chained launches use
+    lib = _native.load()
+    t, h, w = frames.shape
+    dev = torch.from_numpy(frames).cuda()
+    host = torch.from_numpy(frames).pin_memory()
+    s = torch.cuda.current_stream()
+    seen = {}
+    with Pipeline(params, w, h) as pipe:
+        r, f = ctypes.c_int32(), ctypes.c_int64()
+        tickets = []
+        outs = {}
+        for k in range(t):
+            m = modes[k % len(modes)]
+            if m == "push":
+                while tickets:
+                    _native.check(lib.cw_wait(pipe._h, tickets.pop(0), None, None), pipe._h)
+                _native.check(lib.cw_push_device(pipe._h, ctypes.c_void_p(dev[k].data_ptr()), ctypes.byref(r),
+                                                 ctypes.byref(f), ctypes.c_void_p(s.cuda_stream)), pipe._h)
+                torch.cuda.synchronize()
+                if r.value:
+                    seen[k] = _dev_outputs(lib, pipe, _native)[0].view(np.float32).reshape(h, w).copy()
+            else:
+                tk = ctypes.c_int64()
+                if m == "resident":
+                    rc = lib.cw_submit_resident(pipe._h, ctypes.c_void_p(dev[k].data_ptr()), None, None, None,
+                                                ctypes.byref(tk))
+                else:
+                    o = (torch.zeros((h, w), pin_memory=True), torch.zeros((h, w), pin_memory=True),
+                         torch.zeros((h, w, 2 * pipe._idx_bytes), dtype=torch.uint8, pin_memory=True))
+                    outs[k] = o
+                    rc = lib.cw_submit(pipe._h, ctypes.c_void_p(host[k].data_ptr()), ctypes.c_void_p(o[0].data_ptr()),
+                                       ctypes.c_void_p(o[1].data_ptr()), ctypes.c_void_p(o[2].data_ptr()),
+                                       ctypes.byref(tk))
+                _native.check(rc, pipe._h)
+                tickets.append((tk.value))
+                while len(tickets) > 3:
+                    _native.check(lib.cw_wait(pipe._h, tickets.pop(0), None, None), pipe._h)
+        while tickets:
+            _native.check(lib.cw_wait(pipe._h, tickets.pop(0), None, None), pipe._h)
+        torch.cuda.synchronize()
+        for k, o in outs.items():
+            if k >= params.mz - 1:
+                seen[k] = o[0].numpy().copy()
+        snap = pipe.snapshot()
+        final = _dev_outputs(lib, pipe, _native)
+    return seen, snap, final
+
+
+@pytest.mark.parametrize("shape", [(64, 96), (256, 256), (512, 640)])
+def test_resident_chain_matches_serial_launches(params, shape, monkeypatch):
+    h, w = shape
+    frames = _frames(24, h, w, seed=h)
+    _, snap_a, out_a = _run(params, frames, ["push"], monkeypatch, chain=False)
+    _, snap_b, out_b = _run(params, frames, ["resident"], monkeypatch, chain=True)
+    assert np.array_equal(snap_a, snap_b)
+    for x, y in zip(out_a, out_b):
+        assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("shape", [(64, 96), (512, 640)])
+def test_submit_chain_matches_serial_launches(params, shape, monkeypatch):
+    """cw_submit with host frames and host outputs (process_stream's call):
+    every frame's downloaded residual equals the serialised run's."""
+    h, w = shape
+    frames = _frames(20, h, w, seed=7)
+    seen_a, snap_a, _ = _run(params, frames, ["submit"], monkeypatch, chain=False)
+    seen_b, snap_b, _ = _run(params, frames, ["submit"], monkeypatch, chain=True)
+    assert np.array_equal(snap_a, snap_b)
+    assert sorted(seen_a) == sorted(seen_b) and len(seen_a) >= 10
+    for k in seen_a:
+        assert np.array_equal(seen_a[k], seen_b[k]), k
+
+
+def test_mixed_entry_points_match(params, monkeypatch):
+    """Chained and plain launches interleaved on one pipeline (a chained
+    launch after a plain one, a plain one after a chained one)."""
+    frames = _frames(30, 96, 160, seed=11)
+    seen_a, snap_a, _ = _run(params, frames, ["push"], monkeypatch, chain=False)
+    seen_b, snap_b, _ = _run(params, frames, ["resident", "resident", "submit", "push", "submit", "resident"],
+                             monkeypatch, chain=True)
+    assert np.array_equal(snap_a, snap_b)
+    for k in seen_b:
+        assert np.array_equal(seen_a[k], seen_b[k]), k
+
+
+def test_restore_into_a_chained_stream(params, monkeypatch):
+    """Snapshot after 9 frames, restore into a pipeline that already ran a
+    chained stream (its flags are ahead of the restored frame count)."""
+    import torch
+
+    from paper_1408_3526_b200 import Pipeline, _native
+
+    monkeypatch.setenv("CW_DYN_STATIC", "1")
+    frames = _frames(20, 64, 96, seed=3)
+    _, snap_ref, out_ref = _run(params, frames, ["submit"], monkeypatch, chain=True)
+    lib = _native.load()
+    host = torch.from_numpy(frames).pin_memory()
+    with Pipeline(params, 96, 64) as a:
+        for f in frames[:9]:
+            a.process_frame(f)
+        snap9 = a.snapshot()
+    with Pipeline(params, 96, 64) as b:
+        for f in frames[:15]:  # run ahead through the chained submit path
+            list(b.process_stream([f]))
+        b.restore(snap9)
+        for k in range(9, 20):
+            tk = ctypes.c_int64()
+            o = torch.zeros((64, 96), pin_memory=True)
+            _native.check(lib.cw_submit(b._h, ctypes.c_void_p(host[k].data_ptr()), ctypes.c_void_p(o.data_ptr()),
+                                        None, None, ctypes.byref(tk)), b._h)
+            _native.check(lib.cw_wait(b._h, tk.value, None, None), b._h)
+        torch.cuda.synchronize()
+        assert np.array_equal(b.snapshot(), snap_ref)

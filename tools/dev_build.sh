@@ -1,5 +1,5 @@
 #!/bin/bash
-# Fast dev build: only the default geometry (4,4,2,3,3) with 17 lags (+ the
+# Fast dev build: only the default geometry (4,4,2,3,3) with 17 and 33 lags (+ the
 # runtime-loop instance).  Output: $1 (default build/libcw_dev.so); use with
 # CW_B200_LIB=... .  Extra nvcc flags follow the output path.  Prints the
 # frame kernels' register / spill report.
