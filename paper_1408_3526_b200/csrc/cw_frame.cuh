@@ -99,62 +99,12 @@ constexpr int RESTART = CW_RESTART;  // rows between direct y-SDFT restarts (bou
 #ifndef CW_JQ_WIDE
 #define CW_JQ_WIDE 1  // lag column pairs per contraction group for grids of more than 17 lags (2: 1.73 vs 1.27 ms, C5 lag 1/8)
 #endif
-#ifndef CW_WIDE_SPLIT
-#define CW_WIDE_SPLIT 1  // grids of more than 17 lags: balanced schedule with half pairs (wide_split)
+#ifndef CW_PQ_UNROLL_WIDE
+#define CW_PQ_UNROLL_WIDE 16  // unroll of the stage-2 lag loop for grids of more than 17 lags
 #endif
 #ifndef CW_ROLL_WIDE
 #define CW_ROLL_WIDE 1  // the group loop of grids of more than 17 lags is not unrolled (instruction cache)
 #endif
-
-// Contraction schedule for wide symmetric grids (C0 = NL/2 lag column pairs
-// C0 +- q, q = 1..C0, plus the centre pair q = 0): per warp a list of items,
-// byte (q << 2 | half) (half 0: the whole pair, 1: its stage-2 lag rows
-// 1..C0/2, 2: rows C0/2+1..C0), 0xff-terminated, one 64-bit word per warp.
-// Greedy onto the least loaded warp (the last warp, which also runs the next
-// row's x stage, starts half a pair behind); a pair that would take its
-// warp past the even share is split into its two halves (stage 1 runs in
-// both).  33 lags over 5 warps: at most 3.5 pairs per warp instead of 4.
-struct WideSplit {
-    unsigned long long code[8];
-    bool ok;
-};
-__host__ __device__ constexpr WideSplit wide_split(int c0, int nr)
-{
-    WideSplit s{};
-    int load[8] = {}, n[8] = {};
-    for (int w = 0; w < 8; w++) s.code[w] = ~0ull;
-    s.ok = nr >= 2 && nr <= 8 && c0 >= 2;
-    if (!s.ok) return s;
-    load[nr - 1] = 1;
-    const int share = (2 * (c0 + 1) + 1 + nr - 1) / nr;
-    auto least = [&]() {
-        int b = 0;
-        for (int w = 1; w < nr; w++)
-            if (load[w] < load[b]) b = w;
-        return b;
-    };
-    auto put = [&](int w, int q, int half, int cost) {
-        if (n[w] >= 7) {
-            s.ok = false;
-            return;
-        }
-        s.code[w] &= ~(0xffull << (8 * n[w]));
-        s.code[w] |= (unsigned long long)((q << 2) | half) << (8 * n[w]);
-        n[w]++;
-        load[w] += cost;
-    };
-    for (int i = 1; i <= c0 + 1; i++) {
-        const int q = i <= c0 ? i : 0;  // the centre pair last
-        const int w = least();
-        if (load[w] + 2 <= share) {
-            put(w, q, 0, 2);
-        } else {
-            put(least(), q, 1, 1);
-            put(least(), q, 2, 1);
-        }
-    }
-    return s;
-}
 
 struct alignas(16) LagRec {
     float gain, pad;
@@ -1159,9 +1109,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                     // = e + |o| (the same rounding), -ly on a tie (visited first).
                     constexpr int C0 = NL / 2;
                     constexpr int QPW = (C0 + NR) / NR;  // ceil((C0 + 1) / NR)
-                    // lag rows pq in [lo, hi] of stage 2 (a split pair: each half
-                    // gives a partial in-column argmax, merged by rank like any other)
-                    auto group = [&](auto jq, int q0, int lo, int hi) {
+                    auto group = [&](auto jq, int q0) {
                         constexpr int JQ = decltype(jq)::value;
                         int qs[JQ];
                         float g[JQ];
@@ -1232,32 +1180,28 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                             float e = t.s2v[C0].gain * b0[c];
 #pragma unroll
                             for (int k = 1; k <= KY; k++) e = fmaf(t.s2v[C0].cs[k - 1].x, bq[c][k].r, e);
-                            cv[c] = lo <= 1 ? e : -INFINITY;
+                            cv[c] = e;
                             co[c] = 0.f;
                             cpi[c] = 0;
                         }
-                        auto rows = [&](auto p0c, auto p1c) {  // stage-2 lag rows p0..p1, unrolled
-                            constexpr int P0 = decltype(p0c)::value, P1 = decltype(p1c)::value;
+                        constexpr int PQU = NL > 17 ? CW_PQ_UNROLL_WIDE : (C0 > 0 ? C0 : 1);
+#pragma unroll PQU
+                        for (int pq = 1; pq <= C0; pq++) {
+                            const LagRec &L2 = t.s2v[C0 + pq];
 #pragma unroll
-                            for (int pq = P0; pq <= P1; pq++) {
-                                const LagRec &L2 = t.s2v[C0 + pq];
-#pragma unroll
-                                for (int c = 0; c < 2 * JQ; c++) {
+                            for (int c = 0; c < 2 * JQ; c++) {
                                     // (e, o) = (g b0 + sum c Re B, sum s Im B); scores e -+ o
-                                    cf eo = cmk(L2.gain * b0[c], 0.f);
+                                cf eo = cmk(L2.gain * b0[c], 0.f);
 #pragma unroll
-                                    for (int k = 1; k <= KY; k++) eo = cfma2(c2(L2.cs[k - 1]), bq[c][k], eo);
-                                    const float m = eo.r + fabsf(eo.i);
-                                    if (m > cv[c]) {
-                                        cv[c] = m;
-                                        cpi[c] = pq;
-                                        co[c] = eo.i;
-                                    }
+                                for (int k = 1; k <= KY; k++) eo = cfma2(c2(L2.cs[k - 1]), bq[c][k], eo);
+                                const float m = eo.r + fabsf(eo.i);
+                                if (m > cv[c]) {
+                                    cv[c] = m;
+                                    cpi[c] = pq;
+                                    co[c] = eo.i;
                                 }
                             }
-                        };
-                        if (lo <= 1) rows(std::integral_constant<int, 1>{}, std::integral_constant<int, C0 / 2>{});
-                        if (hi > C0 / 2) rows(std::integral_constant<int, C0 / 2 + 1>{}, std::integral_constant<int, C0>{});
+                        }
 #pragma unroll
                         for (int c = 0; c < 2 * JQ; c++) {
                             const int lx = (c & 1) ? C0 - qs[c >> 1] : C0 + qs[c >> 1];
@@ -1266,20 +1210,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                             if (better(cv[c], rk, best, brk)) { best = cv[c]; brk = rk; }
                         }
                     };
-                    constexpr WideSplit WS = wide_split(C0, NR);
-                    if (NL > 17 && CW_WIDE_SPLIT && WS.ok) {
-                        // balanced: pairs and half pairs (wide_split), one rolled loop
-                        unsigned long long code = WS.code[0];
-#pragma unroll
-                        for (int w = 1; w < NR; w++)
-                            if (r == w) code = WS.code[w];
-#pragma unroll 1
-                        for (; (code & 0xffu) != 0xffu; code >>= 8) {
-                            const int q = (int)(code & 0xffu) >> 2, half = (int)(code & 3u);
-                            group(std::integral_constant<int, 1>{}, q, half == 2 ? C0 / 2 + 1 : 1,
-                                  half == 1 ? C0 / 2 : C0);
-                        }
-                    } else {
+                    {
                         constexpr int JW = NL > 17 ? CW_JQ_WIDE : 2;
                         constexpr int NG2 = QPW / JW;
                         // (a group's first pair q0 is on the grid; JW = 1: the last
@@ -1288,16 +1219,16 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
 #pragma unroll 1
                             for (int i = 0; i < NG2; i++)
                                 if (JW == 2 || r + i * NR <= C0)
-                                    group(std::integral_constant<int, JW>{}, r + JW * i * NR, 1, C0);
+                                    group(std::integral_constant<int, JW>{}, r + JW * i * NR);
                         } else {
 #pragma unroll
                             for (int i = 0; i < NG2; i++)
                                 if (JW == 2 || r + i * NR <= C0)
-                                    group(std::integral_constant<int, JW>{}, r + JW * i * NR, 1, C0);
+                                    group(std::integral_constant<int, JW>{}, r + JW * i * NR);
                         }
                         if (JW == 2 && (QPW & 1)) {
                             const int q0 = r + (QPW - 1) * NR;
-                            if (q0 <= C0) group(std::integral_constant<int, 1>{}, q0, 1, C0);
+                            if (q0 <= C0) group(std::integral_constant<int, 1>{}, q0);
                         }
                     }
                 } else {
