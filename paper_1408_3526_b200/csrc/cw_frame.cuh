@@ -102,6 +102,9 @@ constexpr int RESTART = CW_RESTART;  // rows between direct y-SDFT restarts (bou
 #ifndef CW_PQ_UNROLL_WIDE
 #define CW_PQ_UNROLL_WIDE 16  // unroll of the stage-2 lag loop for grids of more than 17 lags
 #endif
+#ifndef CW_ARGMAX_ONLY
+#define CW_ARGMAX_ONLY 0  // diagnostic build: stage-2 lag scores without their FMAs (what a tensor-core contraction would leave)
+#endif
 #ifndef CW_ROLL_WIDE
 #define CW_ROLL_WIDE 1  // the group loop of grids of more than 17 lags is not unrolled (instruction cache)
 #endif
@@ -1192,8 +1195,12 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                             for (int c = 0; c < 2 * JQ; c++) {
                                     // (e, o) = (g b0 + sum c Re B, sum s Im B); scores e -+ o
                                 cf eo = cmk(L2.gain * b0[c], 0.f);
+                                if (CW_ARGMAX_ONLY) {  // diagnostic: the stage-2 FMAs left out (tensor-core bound)
+                                    eo.i = L2.cs[0].y * bq[c][1 + (pq % KY)].i;
+                                } else {
 #pragma unroll
-                                for (int k = 1; k <= KY; k++) eo = cfma2(c2(L2.cs[k - 1]), bq[c][k], eo);
+                                    for (int k = 1; k <= KY; k++) eo = cfma2(c2(L2.cs[k - 1]), bq[c][k], eo);
+                                }
                                 const float m = eo.r + fabsf(eo.i);
                                 if (m > cv[c]) {
                                     cv[c] = m;
