@@ -159,3 +159,49 @@ def test_restore_into_a_chained_stream(params, monkeypatch):
             _native.check(lib.cw_wait(b._h, tk.value, None, None), b._h)
         torch.cuda.synchronize()
         assert np.array_equal(b.snapshot(), snap_ref)
+
+
+def test_two_chained_pipelines_interleaved(params, monkeypatch):
+    """Two pipelines on one GPU, their chained submissions interleaved frame
+    by frame: each stream's state equals its own serialised run (the flags
+    are per pipeline; a spinning CTA of one never waits on the other)."""
+    import torch
+
+    from paper_1408_3526_b200 import Pipeline, _native
+
+    fa = _frames(16, 256, 256, seed=21)
+    fb = _frames(16, 96, 160, seed=22)
+    _, snap_a, _ = _run(params, fa, ["push"], monkeypatch, chain=False)
+    _, snap_b, _ = _run(params, fb, ["push"], monkeypatch, chain=False)
+    monkeypatch.setenv("CW_CHAIN", "1")
+    lib = _native.load()
+    da, db = torch.from_numpy(fa).cuda(), torch.from_numpy(fb).cuda()
+    with Pipeline(params, 256, 256) as a, Pipeline(params, 160, 96) as b:
+        for k in range(16):
+            for pipe, dev in ((a, da), (b, db)):
+                tk = ctypes.c_int64()
+                _native.check(lib.cw_submit_resident(pipe._h, ctypes.c_void_p(dev[k].data_ptr()), None, None, None,
+                                                     ctypes.byref(tk)), pipe._h)
+        torch.cuda.synchronize()
+        assert np.array_equal(a.snapshot(), snap_a)
+        assert np.array_equal(b.snapshot(), snap_b)
+
+
+def test_process_stream_pageable_frames_chained(params, monkeypatch):
+    """process_stream (cw_submit, chained by default) with ordinary pageable
+    numpy frames gives the synchronous process_frame results bit for bit
+    (static split on both)."""
+    from paper_1408_3526_b200 import Pipeline
+
+    monkeypatch.setenv("CW_DYN_STATIC", "1")
+    frames = _frames(14, 128, 192, seed=9)
+    with Pipeline(params, 192, 128) as p1:
+        ref = [p1.process_frame(f) for f in frames]
+    with Pipeline(params, 192, 128) as p2:
+        got = list(p2.process_stream(list(frames)))
+    ref = [r for r in ref if r is not None]
+    assert len(ref) == len(got) == 14 - params.mz + 1
+    for x, y in zip(ref, got):
+        assert x.frame_index == y.frame_index
+        assert np.array_equal(x.residual, y.residual)
+        assert np.array_equal(x.velocity.indices, y.velocity.indices)
