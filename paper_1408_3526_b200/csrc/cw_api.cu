@@ -127,6 +127,7 @@ struct cw_handle {
     int ready_of[NEV] = {};
     long long fidx_of[NEV] = {};
     bool dl_flagged[NEV] = {};  // chained cw_submit: the frame's download is followed by a flag write
+    bool dl_any[NEV] = {};      // the frame's outputs were downloaded on `down` (its output set is busy)
     // detection epilogue: 2 device sets (double-buffered like the outputs),
     // NEV pinned host mirrors (one per outstanding frame)
     float det_tau = 0.f;
@@ -868,6 +869,7 @@ static int run_frame(cw_handle *h, cudaStream_t s, int32_t *ready, int64_t *fram
     chain = chain && chained(h);
     const bool pdl = chain && h->last_static;
     h->dl_flagged[h->frames_seen % cw_handle::NEV] = false;  // set again by a flagged cw_submit
+    h->dl_any[h->frames_seen % cw_handle::NEV] = false;
     NvtxRange nvtx("cw_frame");
     const size_t HW = (size_t)h->W * h->H;
     const long long n = h->frames_seen;
@@ -912,8 +914,10 @@ static int run_frame(cw_handle *h, cudaStream_t s, int32_t *ready, int64_t *fram
     a.up_flag = a.down_flag = nullptr;
     a.up_want = a.down_want = 0;
     if (flags) {
-        a.up_flag = h->d_flags;
-        a.up_want = flags->up_want;
+        if (flags->up_want) {
+            a.up_flag = h->d_flags;
+            a.up_want = flags->up_want;
+        }
         if (flags->down_want) {
             a.down_flag = h->d_flags + 1;
             a.down_want = flags->down_want;
@@ -1321,8 +1325,12 @@ static int submit_impl(cw_handle *h, const void *samples, int format, double sca
             CUDA_SUCCESS)
             return fail(h, CW_ERR_CUDA, "cuStreamWriteValue32 failed");
         fw.up_want = tag;
-        // frame n - 2 wrote this output set; its download posted n - 1
-        fw.down_want = (n >= 2 && h->dl_flagged[(n - 2) % cw_handle::NEV]) ? (unsigned int)(n - 1) : 0u;
+        // frame n - 2 wrote this output set: a flagged download posted n - 1,
+        // any other download is waited for by its event
+        if (n >= 2 && h->dl_flagged[(n - 2) % cw_handle::NEV])
+            fw.down_want = (unsigned int)(n - 1);
+        else if (n >= 2 && h->dl_any[(n - 2) % cw_handle::NEV])
+            CW_CUDA(h, cudaStreamWaitEvent(h->own, h->ev_down[(n - 2) % cw_handle::NEV], 0));
     } else {
         CW_CUDA(h, cudaStreamWaitEvent(h->own, h->ev_up[e], 0));
         if (n >= 2)
@@ -1344,6 +1352,7 @@ static int submit_impl(cw_handle *h, const void *samples, int format, double sca
         if (vidx)
             CW_CUDA(h, cudaMemcpyAsync(vidx, h->d_vidx + set * HW * 2 * h->idx_bytes, HW * 2 * h->idx_bytes, cudaMemcpyDeviceToHost, h->down));
     }
+    h->dl_any[e] = rd && (residual || prediction || vidx);
     if (flagged) {
         if (h->write_value(reinterpret_cast<CUstream>(h->down), reinterpret_cast<CUdeviceptr>(h->d_flags + 1),
                            (unsigned int)(n + 1), 0) != CUDA_SUCCESS)
@@ -1406,15 +1415,26 @@ static int submit_device_impl(cw_handle *h, const float *frame_dev, float *resid
         CW_CUDA(h, cudaStreamWaitEvent(ps, h->ev_up[e], 0));
     }
     // the output set of frame n - 2 is downloaded before kernel n rewrites
-    // it; with no host outputs there is no download, and no wait: a pending
-    // cross-stream wait between two frame kernels would serialise them
+    // it.  Chained: a flagged download is waited for in the kernel, another
+    // download by its event, no download not at all -- a pending
+    // cross-stream wait between two frame kernels serialises them
     // (measured: it cancels the programmatic launch)
-    if (n >= 2 && (residual || prediction || vidx || !resident))
-        CW_CUDA(h, cudaStreamWaitEvent(h->own, h->ev_down[(n - 2) % cw_handle::NEV], 0));
+    FlagWants fw{};
+    bool use_fw = false;
+    if (n >= 2) {
+        const int e2 = (int)((n - 2) % cw_handle::NEV);
+        if (resident && h->dl_flagged[e2]) {
+            fw.down_want = (unsigned int)(n - 1);
+            use_fw = true;
+        } else if (!resident || h->dl_any[e2]) {
+            CW_CUDA(h, cudaStreamWaitEvent(h->own, h->ev_down[e2], 0));
+        }
+    }
     int32_t rd = 0;
     int64_t fi = -1;
     const size_t set = (size_t)(n & 1);
-    int rc = run_frame(h, h->own, &rd, &fi, nullptr, nullptr, nullptr, resident ? frame_dev : nullptr, resident);
+    int rc = run_frame(h, h->own, &rd, &fi, nullptr, nullptr, nullptr, resident ? frame_dev : nullptr, resident,
+                       use_fw ? &fw : nullptr);
     if (rc != CW_OK)
         return rc;
     CW_CUDA(h, cudaEventRecord(h->ev_k[e], h->own));
@@ -1428,6 +1448,7 @@ static int submit_device_impl(cw_handle *h, const float *frame_dev, float *resid
         if (vidx)
             CW_CUDA(h, cudaMemcpyAsync(vidx, h->d_vidx + set * vb, vb, cudaMemcpyDeviceToHost, h->down));
     }
+    h->dl_any[e] = rd && (residual || prediction || vidx);
     CW_CUDA(h, cudaEventRecord(h->ev_down[e], h->down));
     h->ready_of[e] = rd;
     h->fidx_of[e] = fi;
@@ -1603,6 +1624,8 @@ int cw_restore(cw_handle *h, const void *src, size_t bytes)
     if (h->d_flags)
         CW_CUDA(h, cudaMemset(h->d_flags, 0, 2 * sizeof(unsigned int)));
     for (bool &f : h->dl_flagged)
+        f = false;
+    for (bool &f : h->dl_any)
         f = false;
     return CW_OK;
 }

@@ -205,3 +205,56 @@ def test_process_stream_pageable_frames_chained(params, monkeypatch):
         assert x.frame_index == y.frame_index
         assert np.array_equal(x.residual, y.residual)
         assert np.array_equal(x.velocity.indices, y.velocity.indices)
+
+
+def test_mixed_download_kinds_guard_the_output_sets(params, monkeypatch):
+    """Downloads of different kinds two frames apart: a chained cw_submit
+    after an event-only (PGM16) download of the same output set, and a
+    resident frame after a flagged download -- every downloaded residual
+    equals the serialised run's."""
+    import torch
+
+    from paper_1408_3526_b200 import Pipeline, _native
+
+    monkeypatch.setenv("CW_DYN_STATIC", "1")
+    frames = _frames(24, 64, 96, seed=13)
+    q = np.clip(np.rint((frames - 9.0) / 2.0 * 65535.0), 0, 65535).astype(">u2")
+    scale, offset = 2.0 / 65535.0, 9.0
+    deq = (q.astype(np.float64) * scale + offset).astype(np.float32)
+    seen_a, snap_a, _ = _run(params, deq, ["submit"], monkeypatch, chain=False)
+    monkeypatch.setenv("CW_CHAIN", "1")
+    lib = _native.load()
+    dev = torch.from_numpy(deq).cuda()
+    host = torch.from_numpy(deq).pin_memory()
+    seen = {}
+    with Pipeline(params, 96, 64) as pipe:
+        tickets, outs = [], {}
+        for k in range(24):
+            tk = ctypes.c_int64()
+            o = torch.zeros((64, 96), pin_memory=True)
+            m = ("pgm", "pgm", "f32", "f32", "res", "res")[k % 6]
+            if m == "pgm":
+                raw = np.ascontiguousarray(q[k])
+                rc = lib.cw_submit_raw(pipe._h, raw.ctypes.data, _native.FMT_PGM16, scale, offset,
+                                       ctypes.c_void_p(o.data_ptr()), None, None, ctypes.byref(tk))
+                outs[k] = (o, raw)
+            elif m == "f32":
+                rc = lib.cw_submit(pipe._h, ctypes.c_void_p(host[k].data_ptr()), ctypes.c_void_p(o.data_ptr()),
+                                   None, None, ctypes.byref(tk))
+                outs[k] = (o, None)
+            else:
+                rc = lib.cw_submit_resident(pipe._h, ctypes.c_void_p(dev[k].data_ptr()), None, None, None,
+                                            ctypes.byref(tk))
+            _native.check(rc, pipe._h)
+            tickets.append(tk.value)
+            while len(tickets) > 3:
+                _native.check(lib.cw_wait(pipe._h, tickets.pop(0), None, None), pipe._h)
+        while tickets:
+            _native.check(lib.cw_wait(pipe._h, tickets.pop(0), None, None), pipe._h)
+        torch.cuda.synchronize()
+        for k, (o, _) in outs.items():
+            if k >= params.mz - 1:
+                seen[k] = o.numpy().copy()
+        assert np.array_equal(pipe.snapshot(), snap_a)
+    for k in seen:
+        assert np.array_equal(seen[k], seen_a[k]), k
