@@ -654,7 +654,10 @@ int cw_create(const cw_params *p, int32_t width, int32_t height, int32_t device,
         if (occ < 1 || sms < 1)
             return cleanup_fail(CW_ERR_CUDA, "frame kernel cannot be resident on this device");
         const long long units = (long long)h->NXB * (height - halo_rows);
-        h->grid = (int)std::min<long long>((long long)occ * sms, std::max<long long>(1, units / 2));
+        long long slots = (long long)occ * sms;
+        if (const char *e = std::getenv("CW_GRID_X"))  // experiment knob: CTAs per resident slot
+            slots = std::max<long long>(1, (long long)(std::atof(e) * (double)slots));
+        h->grid = (int)std::min<long long>(slots, std::max<long long>(1, units / 2));
     }
     h->sms = std::max(1, sms);
 

@@ -105,6 +105,9 @@ constexpr int RESTART = CW_RESTART;  // rows between direct y-SDFT restarts (bou
 #ifndef CW_ARGMAX_ONLY
 #define CW_ARGMAX_ONLY 0  // diagnostic build: stage-2 lag scores without their FMAs (what a tensor-core contraction would leave)
 #endif
+#ifndef CW_EARLY_PREROLL
+#define CW_EARLY_PREROLL 1  // chained launches: first run's x-stage pre-roll before the wait for the previous frame
+#endif
 #ifndef CW_ROLL_WIDE
 #define CW_ROLL_WIDE 1  // the group loop of grids of more than 17 lags is not unrolled (instruction cache)
 #endif
@@ -598,7 +601,13 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
         const size_t n = (size_t)W * H, b0 = n * blockIdx.x / gridDim.x, b1 = n * (blockIdx.x + 1) / gridDim.x;
         for (size_t i = b0 + threadIdx.x; i < b1; i += G::NTHREADS) a.ring_dst[i] = __ldg(a.frame + i);
     }
-    if (a.done && threadIdx.x == G::NTHREADS - 32) chain_wait(a.done + blockIdx.x, a.seq - 1u);  // the TMA issuer
+    // the TMA issuer waits for this CTA's units of the previous frame -- here,
+    // or (CW_EARLY_PREROLL) after the first run's x-stage pre-roll, which
+    // reads only the current frame (wide lag grids: the plain order, which
+    // their register allocation prefers)
+    constexpr bool EARLY = CW_EARLY_PREROLL && NL <= 17;
+    bool chain_pending = EARLY && a.done != nullptr;
+    if (!EARLY && a.done && threadIdx.x == G::NTHREADS - 32) chain_wait(a.done + blockIdx.x, a.seq - 1u);
     __syncthreads();
     uint32_t phase = 0, phase_t = 0;
 
@@ -713,11 +722,19 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
 
         if (CW_FENCE_ALL) fence_proxy_async();
         __syncthreads();  // previous chunk done with the stage and the ring
-        issue(ys, xb);
-        issue_t(ys, xb);
+        if (!chain_pending) {
+            issue(ys, xb);
+            issue_t(ys, xb);
+        }
         for (int k = r; k < MY; k += NR) {
             const int yy = ys - MY + 1 + k;
             xstage(yy, x, ring_slot(yy));
+        }
+        if (chain_pending) {  // first run: the packets after the previous frame's
+            if (threadIdx.x == G::NTHREADS - 32) chain_wait(a.done + blockIdx.x, a.seq - 1u);
+            issue(ys, xb);
+            issue_t(ys, xb);
+            chain_pending = false;
         }
         __syncthreads();
 
