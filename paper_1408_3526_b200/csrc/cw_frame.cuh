@@ -472,7 +472,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase)
 // per-warp clock64 accumulators (phase-timing builds only): [warp][event]
 __device__ unsigned long long cw_phase_clk[8][16];
 // per-CTA %globaltimer (ns) at kernel entry and exit, last launch: [cta][2]
-__device__ unsigned long long cw_cta_span[1024][2];
+// [seq & 1][CTA]: start, setup done, ring copy done, pre-roll done, chain wait done, end
+__device__ unsigned long long cw_cta_span[2][1024][6];
 __device__ __forceinline__ unsigned long long cw_gtimer()
 {
     unsigned long long t;
@@ -538,7 +539,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
 #ifdef CW_PHASE_TIMING
     unsigned long long clk_prev = cw_clock_pinned();
     unsigned long long clk_acc[11] = {};
-    if (threadIdx.x == 0 && blockIdx.x < 1024) cw_cta_span[blockIdx.x][0] = cw_gtimer();
+    if (threadIdx.x == 0 && blockIdx.x < 1024) cw_cta_span[a.seq & 1][blockIdx.x][0] = cw_gtimer();
 #endif
     constexpr int KX = G::KX, KY = G::KY, KZ = G::KZ, BX = G::BX, BY = G::BY;
     constexpr int MX = G::MX, MY = G::MY, MZ = G::MZ;
@@ -590,17 +591,61 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
     if (a.work && blockIdx.x == 0 && threadIdx.x == 0) a.work[a.parity ^ 1] = 0u;
     // the next frame's launch may start now (it waits on done[] per CTA)
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#ifdef CW_PHASE_TIMING
+    if (threadIdx.x == 0 && blockIdx.x < 1024) cw_cta_span[a.seq & 1][blockIdx.x][1] = cw_gtimer();
+#endif
     if ((a.up_flag || a.down_flag) && threadIdx.x == G::NTHREADS - 32) {
         if (a.up_flag) chain_wait(a.up_flag, a.up_want);
         if (a.down_flag) chain_wait(a.down_flag, a.down_want);
     }
     if (a.ring_dst) {
-        if (r == KY)
-            for (int j = lane; j < (int)gridDim.x; j += 32) chain_wait(a.done + j, a.seq - 2u);
-        __syncthreads();
-        const size_t n = (size_t)W * H, b0 = n * blockIdx.x / gridDim.x, b1 = n * (blockIdx.x + 1) / gridDim.x;
-        for (size_t i = b0 + threadIdx.x; i < b1; i += G::NTHREADS) a.ring_dst[i] = __ldg(a.frame + i);
+        // every CTA of launch seq - 2 through: all flags read at once (relaxed,
+        // then a fence before the barrier: acquire for the whole CTA), retried
+        // while one is behind -- one L2 round trip, not one per flag
+        for (long long it = 0;; it++) {
+            bool ok = true;
+            for (int j = threadIdx.x; j < (int)gridDim.x; j += G::NTHREADS) {
+                unsigned int v;
+                asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.done + j) : "memory");
+                ok = ok && (int)(v - (a.seq - 2u)) >= 0;
+            }
+            __threadfence();
+            if (__syncthreads_and(ok)) break;
+            if (it > (1ll << 22)) asm volatile("trap;");
+            __nanosleep(256);
+        }
+        // this CTA's share of the frame, 16-byte vectors when aligned; all
+        // loads of a thread issued before its stores (a handful per thread).
+        // (Writing each CTA's own units' pixels per row from the x-stage row
+        // segments instead measured slower: the store lands on warp KY's
+        // critical path.)
+        const size_t n = (size_t)W * H;
+        if ((n & 3) == 0 && ((reinterpret_cast<uintptr_t>(a.frame) | reinterpret_cast<uintptr_t>(a.ring_dst)) & 15) == 0) {
+            const size_t n4 = n / 4, b0 = n4 * blockIdx.x / gridDim.x, b1 = n4 * (blockIdx.x + 1) / gridDim.x;
+            const float4 *src = reinterpret_cast<const float4 *>(a.frame);
+            float4 *dst = reinterpret_cast<float4 *>(a.ring_dst);
+            constexpr int U = 4;
+            for (size_t i = b0 + threadIdx.x; i < b1; i += U * G::NTHREADS) {
+                float4 v[U];
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const size_t k = i + (size_t)u * G::NTHREADS;
+                    if (k < b1) v[u] = __ldg(src + k);
+                }
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const size_t k = i + (size_t)u * G::NTHREADS;
+                    if (k < b1) dst[k] = v[u];
+                }
+            }
+        } else {
+            const size_t b0 = n * blockIdx.x / gridDim.x, b1 = n * (blockIdx.x + 1) / gridDim.x;
+            for (size_t i = b0 + threadIdx.x; i < b1; i += G::NTHREADS) a.ring_dst[i] = __ldg(a.frame + i);
+        }
     }
+#ifdef CW_PHASE_TIMING
+    if (threadIdx.x == 0 && blockIdx.x < 1024) cw_cta_span[a.seq & 1][blockIdx.x][2] = cw_gtimer();
+#endif
     // the TMA issuer waits for this CTA's units of the previous frame -- here,
     // or (CW_EARLY_PREROLL) after the first run's x-stage pre-roll, which
     // reads only the current frame (wide lag grids: the plain order, which
@@ -731,7 +776,15 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
             xstage(yy, x, ring_slot(yy));
         }
         if (chain_pending) {  // first run: the packets after the previous frame's
-            if (threadIdx.x == G::NTHREADS - 32) chain_wait(a.done + blockIdx.x, a.seq - 1u);
+            if (threadIdx.x == G::NTHREADS - 32) {
+#ifdef CW_PHASE_TIMING
+                if (blockIdx.x < 1024) cw_cta_span[a.seq & 1][blockIdx.x][3] = cw_gtimer();
+#endif
+                chain_wait(a.done + blockIdx.x, a.seq - 1u);
+#ifdef CW_PHASE_TIMING
+                if (blockIdx.x < 1024) cw_cta_span[a.seq & 1][blockIdx.x][4] = cw_gtimer();
+#endif
+            }
             issue(ys, xb);
             issue_t(ys, xb);
             chain_pending = false;
@@ -1393,7 +1446,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
     if (blockIdx.x == 0 && (threadIdx.x & 31) == 0)
         for (int k = 0; k < 11; k++) cw_phase_clk[threadIdx.x >> 5][k] += clk_acc[k];
     __syncthreads();
-    if (threadIdx.x == 0 && blockIdx.x < 1024) cw_cta_span[blockIdx.x][1] = cw_gtimer();
+    if (threadIdx.x == 0 && blockIdx.x < 1024) cw_cta_span[a.seq & 1][blockIdx.x][5] = cw_gtimer();
 #endif
 #undef XFR
 }

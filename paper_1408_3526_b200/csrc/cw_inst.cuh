@@ -24,11 +24,11 @@ struct LaunchFn {
 };
 
 #ifdef CW_PHASE_TIMING
-static void phase_clocks_read(unsigned long long *dst)  // [8][16] + CTA spans [1024][2], clocks zeroed
+static void phase_clocks_read(unsigned long long *dst)  // [8][16] + CTA spans [2][1024][6], clocks zeroed
 {
     cudaDeviceSynchronize();
     cudaMemcpyFromSymbol(dst, cw_phase_clk, sizeof(unsigned long long) * 128);
-    cudaMemcpyFromSymbol(dst + 128, cw_cta_span, sizeof(unsigned long long) * 2048);
+    cudaMemcpyFromSymbol(dst + 128, cw_cta_span, sizeof(unsigned long long) * 12288);
     static unsigned long long zero[128] = {};
     cudaMemcpyToSymbol(cw_phase_clk, zero, sizeof zero);
 }
