@@ -1452,6 +1452,14 @@ static int submit_device_impl(cw_handle *h, const float *frame_dev, float *resid
             CW_CUDA(h, cudaMemcpyAsync(vidx, h->d_vidx + set * vb, vb, cudaMemcpyDeviceToHost, h->down));
     }
     h->dl_any[e] = rd && (residual || prediction || vidx);
+    if (resident && h->dl_any[e] && h->write_value) {
+        // the next-but-one resident frame waits for this download in its
+        // kernel (flag), not on the kernel stream (event)
+        if (h->write_value(reinterpret_cast<CUstream>(h->down), reinterpret_cast<CUdeviceptr>(h->d_flags + 1),
+                           (unsigned int)(n + 1), 0) != CUDA_SUCCESS)
+            return fail(h, CW_ERR_CUDA, "cuStreamWriteValue32 failed");
+        h->dl_flagged[e] = true;
+    }
     CW_CUDA(h, cudaEventRecord(h->ev_down[e], h->down));
     h->ready_of[e] = rd;
     h->fidx_of[e] = fi;

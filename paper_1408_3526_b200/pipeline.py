@@ -417,6 +417,55 @@ class Pipeline:
                 if self._h:
                     lib.cw_wait(self._h, ticket, None, None)
 
+    def process_resident(self, frames, depth: int = 3):
+        """Pipelined ``process_frame`` over device-resident frames: an
+        iterable of CUDA float32 (H, W) tensors on this pipeline's device,
+        each complete when handed over (the producer is synchronised here)
+        and left unchanged until its output is yielded.  Consecutive frame
+        kernels are chained (cw_submit_resident): no frame
+        copy, and a frame's kernel starts in the SM slots the previous one's
+        early CTAs free.  Yields the WhitenedOutput of every ready frame, in
+        order, with host arrays (downloaded while later frames run)."""
+        import torch
+        from collections import deque
+
+        lib = _native.load()
+        depth = max(1, min(int(depth), 6))
+        h, w = self.height, self.width
+        inflight: deque = deque()
+
+        def collect(item):
+            ticket, _frame, res, pred, vidx = item
+            ready, fidx = ctypes.c_int32(0), ctypes.c_int64(-1)
+            _native.check(lib.cw_wait(self._h, ticket, ctypes.byref(ready), ctypes.byref(fidx)), self._h)
+            return self._wrap(int(fidx.value), res, pred, vidx, ticket=ticket) if ready.value else None
+
+        try:
+            for frame in frames:
+                if (tuple(frame.shape) != (h, w) or frame.dtype != torch.float32 or not frame.is_cuda
+                        or not frame.is_contiguous()):
+                    raise ValueError(f"expected a contiguous CUDA float32 tensor of shape {(h, w)}")
+                torch.cuda.current_stream(frame.device).synchronize()  # the frame is complete
+                res, pred, vidx = self._pool.take_outputs(h, w, self._idx_bytes)
+                ticket = ctypes.c_int64(-1)
+                _native.check(lib.cw_submit_resident(self._h, ctypes.c_void_p(frame.data_ptr()), res.ctypes.data,
+                                                     pred.ctypes.data, vidx.ctypes.data, ctypes.byref(ticket)),
+                              self._h)
+                inflight.append((ticket.value, frame, res, pred, vidx))
+                while len(inflight) > depth:
+                    out = collect(inflight.popleft())
+                    if out is not None:
+                        yield out
+            while inflight:
+                out = collect(inflight.popleft())
+                if out is not None:
+                    yield out
+        finally:
+            while inflight:
+                ticket = inflight.popleft()[0]
+                if self._h:
+                    lib.cw_wait(self._h, ticket, None, None)
+
     def process_frame_device(self, frame) -> WhitenedOutput | None:
         """``process_frame`` for a frame already in device memory: a CUDA
         float32 (H, W) torch tensor on this pipeline's device (e.g. a strip

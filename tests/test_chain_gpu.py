@@ -258,3 +258,26 @@ def test_mixed_download_kinds_guard_the_output_sets(params, monkeypatch):
         assert np.array_equal(pipe.snapshot(), snap_a)
     for k in seen:
         assert np.array_equal(seen[k], seen_a[k]), k
+
+
+def test_process_resident_matches_process_frame(params, monkeypatch):
+    """Pipeline.process_resident (cw_submit_resident with host outputs,
+    chained, flagged downloads) gives the synchronous results bit for bit
+    (static split on both)."""
+    import torch
+
+    from paper_1408_3526_b200 import Pipeline
+
+    monkeypatch.setenv("CW_DYN_STATIC", "1")
+    frames = _frames(16, 96, 160, seed=31)
+    with Pipeline(params, 160, 96) as p1:
+        ref = [o for o in (p1.process_frame(f) for f in frames) if o is not None]
+    dev = [torch.from_numpy(f).cuda() for f in frames]
+    with Pipeline(params, 160, 96) as p2:
+        got = list(p2.process_resident(dev))
+    assert len(ref) == len(got) == 16 - params.mz + 1
+    for x, y in zip(ref, got):
+        assert x.frame_index == y.frame_index
+        assert np.array_equal(x.residual, y.residual)
+        assert np.array_equal(x.prediction, y.prediction)
+        assert np.array_equal(x.velocity.indices, y.velocity.indices)
