@@ -912,7 +912,7 @@ static int run_frame(cw_handle *h, cudaStream_t s, int32_t *ready, int64_t *fram
     a.rxy_g = h->d_rank ? h->d_rank + (size_t)h->nlx * h->nly * 2 : nullptr;
     a.det = nullptr;
     a.done = h->d_done;
-    a.seq = ++h->seq;
+    a.seq = h->seq + 1;  // committed once the launch went in (a failed launch publishes no flags)
     a.ring_dst = nullptr;
     a.up_flag = a.down_flag = nullptr;
     a.up_want = a.down_want = 0;
@@ -1035,6 +1035,7 @@ static int run_frame(cw_handle *h, cudaStream_t s, int32_t *ready, int64_t *fram
         }
         CW_CUDA(h, cudaGetLastError());
         h->last_static = a.work == nullptr;
+        h->seq = a.seq;
     }
     if (h->timing)
         CW_CUDA(h, cudaEventRecord(e1, s));
