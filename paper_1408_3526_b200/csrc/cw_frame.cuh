@@ -108,9 +108,54 @@ constexpr int RESTART = CW_RESTART;  // rows between direct y-SDFT restarts (bou
 #ifndef CW_EARLY_PREROLL
 #define CW_EARLY_PREROLL 1  // chained launches: first run's x-stage pre-roll before the wait for the previous frame
 #endif
+#ifndef CW_SMSP_17
+#define CW_SMSP_17 1  // the 17-lag grid too: one pair per group, dealt by smsp_sched (C3 -1.7%, C2 -4.5%, C5 -1.4..-2.6%)
+#endif
+#ifndef CW_SMSP_SCHED
+#define CW_SMSP_SCHED 1  // grids of more than 17 lags: lag column pairs dealt by scheduler load (smsp_sched)
+#endif
 #ifndef CW_ROLL_WIDE
 #define CW_ROLL_WIDE 1  // the group loop of grids of more than 17 lags is not unrolled (instruction cache)
 #endif
+
+// Lag column pairs of a wide symmetric grid (q = 0..C0; q = 0 is the
+// centre column) dealt to the NR warps of a CTA by scheduler load: warp w
+// issues on sub-partition w % 4, so with NR = 5 warps 0 and NR-1 share one
+// scheduler in every phase.  Greedy: each pair goes to the warp whose
+// scheduler has the least work (the last warp carries the next row's x
+// stage as half a pair), ties to the warp with fewer pairs.  33 lags, 5
+// warps: pairs 3/4/4/4/2 (scheduler loads 5.5/4/4/4) instead of round
+// robin's 4/4/3/3/3 (7.5/4/3/3).  Per warp a list of q, 5 bits each,
+// terminated by 31, one 32-bit word per warp (at most 6 pairs).
+struct SmspSched {
+    unsigned int code[8];
+    bool ok;
+};
+__host__ __device__ constexpr SmspSched smsp_sched(int c0, int nr)
+{
+    SmspSched s{};
+    int n[8] = {}, load2[4] = {};  // pairs per warp; scheduler load in half pairs
+    for (int w = 0; w < 8; w++) s.code[w] = ~0u;
+    s.ok = nr >= 2 && nr <= 8 && c0 < 31;
+    if (!s.ok) return s;
+    load2[(nr - 1) % 4] += 1;
+    for (int q = 0; q <= c0; q++) {
+        int b = 0;
+        for (int w = 1; w < nr; w++) {
+            const int lw = load2[w % 4], lb = load2[b % 4];
+            if (lw < lb || (lw == lb && n[w] < n[b])) b = w;
+        }
+        if (n[b] >= 6) {
+            s.ok = false;
+            return s;
+        }
+        s.code[b] &= ~(31u << (5 * n[b]));
+        s.code[b] |= (unsigned int)q << (5 * n[b]);
+        n[b]++;
+        load2[b % 4] += 2;
+    }
+    return s;
+}
 
 struct alignas(16) LagRec {
     float gain, pad;
@@ -1288,11 +1333,22 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                         }
                     };
                     {
-                        constexpr int JW = NL > 17 ? CW_JQ_WIDE : 2;
+                        constexpr bool SMSP17 = CW_SMSP_17 && NL == 17;
+                        constexpr int JW = NL > 17 ? CW_JQ_WIDE : (SMSP17 ? 1 : 2);
                         constexpr int NG2 = QPW / JW;
                         // (a group's first pair q0 is on the grid; JW = 1: the last
                         // round of q can run past it and is skipped)
-                        if (NL > 17 && CW_ROLL_WIDE) {
+                        constexpr SmspSched SS = smsp_sched(C0, NR);
+                        if ((NL > 17 || SMSP17) && JW == 1 && CW_ROLL_WIDE && CW_SMSP_SCHED && SS.ok) {
+                            // whole pairs dealt by scheduler load (smsp_sched)
+                            unsigned int code = SS.code[0];
+#pragma unroll
+                            for (int w = 1; w < NR; w++)
+                                if (r == w) code = SS.code[w];
+#pragma unroll 1
+                            for (; (code & 31u) != 31u; code >>= 5)
+                                group(std::integral_constant<int, 1>{}, (int)(code & 31u));
+                        } else if (NL > 17 && CW_ROLL_WIDE) {
 #pragma unroll 1
                             for (int i = 0; i < NG2; i++)
                                 if (JW == 2 || r + i * NR <= C0)
