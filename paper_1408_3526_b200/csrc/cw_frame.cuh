@@ -111,6 +111,9 @@ constexpr int RESTART = CW_RESTART;  // rows between direct y-SDFT restarts (bou
 #ifndef CW_SMSP_17
 #define CW_SMSP_17 1  // the 17-lag grid too: one pair per group, dealt by smsp_sched (C3 -1.7%, C2 -4.5%, C5 -1.4..-2.6%)
 #endif
+#ifndef CW_SMSP_9
+#define CW_SMSP_9 0  // the 9-lag grid too
+#endif
 #ifndef CW_SMSP_SCHED
 #define CW_SMSP_SCHED 1  // grids of more than 17 lags: lag column pairs dealt by scheduler load (smsp_sched)
 #endif
@@ -1333,7 +1336,7 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
                         }
                     };
                     {
-                        constexpr bool SMSP17 = CW_SMSP_17 && NL == 17;
+                        constexpr bool SMSP17 = CW_SMSP_17 && (NL == 17 || (CW_SMSP_9 && NL == 9));
                         constexpr int JW = NL > 17 ? CW_JQ_WIDE : (SMSP17 ? 1 : 2);
                         constexpr int NG2 = QPW / JW;
                         // (a group's first pair q0 is on the grid; JW = 1: the last

@@ -57,6 +57,8 @@ CONFIGS = {
     "c5": {"w": 1280, "h": 1024, "params": {}},
     "c5lag8": {"w": 1280, "h": 1024, "params": {"lag_grid_x": tuple(i / 8 for i in range(-16, 17)),
                                                  "lag_grid_y": tuple(i / 8 for i in range(-16, 17))}},
+    "c5lag2": {"w": 1280, "h": 1024, "params": {"lag_grid_x": tuple(i / 2 for i in range(-4, 5)),
+                                                 "lag_grid_y": tuple(i / 2 for i in range(-4, 5))}},
     "c5k5": {"w": 1280, "h": 1024, "params": {"kx": 5, "ky": 5, "bx": 4, "by": 4, "mhat": (5, 5, 2)}},
     "c5k3": {"w": 1280, "h": 1024, "params": {"kx": 3, "ky": 3, "bx": 2, "by": 2, "mhat": (3, 3, 2)}},
     "c5kz1": {"w": 1280, "h": 1024, "params": {"kz": 1, "mhat": (4, 4, 1)}},
