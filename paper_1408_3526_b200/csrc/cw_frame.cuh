@@ -111,6 +111,9 @@ constexpr int RESTART = CW_RESTART;  // rows between direct y-SDFT restarts (bou
 #ifndef CW_SMSP_17
 #define CW_SMSP_17 1  // the 17-lag grid too: one pair per group, dealt by smsp_sched (C3 -1.7%, C2 -4.5%, C5 -1.4..-2.6%)
 #endif
+#ifndef CW_SMSP_FIX
+#define CW_SMSP_FIX 1  // smsp_sched: pair counts that also balance the SM-mate CTA (5 warps; C3 -0.8%)
+#endif
 #ifndef CW_SMSP_9
 #define CW_SMSP_9 0  // the 9-lag grid too
 #endif
@@ -121,14 +124,15 @@ constexpr int RESTART = CW_RESTART;  // rows between direct y-SDFT restarts (bou
 #define CW_ROLL_WIDE 1  // the group loop of grids of more than 17 lags is not unrolled (instruction cache)
 #endif
 
-// Lag column pairs of a wide symmetric grid (q = 0..C0; q = 0 is the
-// centre column) dealt to the NR warps of a CTA by scheduler load: warp w
-// issues on sub-partition w % 4, so with NR = 5 warps 0 and NR-1 share one
-// scheduler in every phase.  Greedy: each pair goes to the warp whose
-// scheduler has the least work (the last warp carries the next row's x
-// stage as half a pair), ties to the warp with fewer pairs.  33 lags, 5
-// warps: pairs 3/4/4/4/2 (scheduler loads 5.5/4/4/4) instead of round
-// robin's 4/4/3/3/3 (7.5/4/3/3).  Per warp a list of q, 5 bits each,
+// Lag column pairs of a symmetric grid (q = 0..C0; q = 0 is the centre
+// column) dealt to the NR warps of a CTA by scheduler load: warp w issues
+// on sub-partition w % 4, so with NR = 5 warps 0 and NR-1 share one
+// scheduler in every phase, and the SM-mate CTA's warp w issues on
+// (w + 1) % 4.  Greedy: each pair goes to the warp whose scheduler has the
+// least work (the last warp carries the next row's x stage as half a
+// pair), ties to the warp with fewer pairs, within per-warp caps that also
+// balance the SM-mate's copy (CW_SMSP_FIX).  33 lags, 5 warps: pairs
+// 2/4/5/4/2 instead of round robin's 4/4/3/3/3.  Per warp a list of q, 5 bits each,
 // terminated by 31, one 32-bit word per warp (at most 6 pairs).
 struct SmspSched {
     unsigned int code[8];
@@ -141,14 +145,26 @@ __host__ __device__ constexpr SmspSched smsp_sched(int c0, int nr)
     for (int w = 0; w < 8; w++) s.code[w] = ~0u;
     s.ok = nr >= 2 && nr <= 8 && c0 < 31;
     if (!s.ok) return s;
+    int cap[8] = {7, 7, 7, 7, 7, 7, 7, 7};  // pairs per warp at most
+    if (CW_SMSP_FIX && nr == 5 && (c0 == 16 || c0 == 8)) {
+        // counts that also balance the SM-mate CTA's schedulers (its warp w
+        // issues on (w + 1) % 4): 33 lags 2/4/5/4/2, 17 lags 1/2/3/2/1
+        const int c16[5] = {2, 4, 5, 4, 2}, c8[5] = {1, 2, 3, 2, 1};
+        for (int w = 0; w < 5; w++) cap[w] = c0 == 16 ? c16[w] : c8[w];
+    }
     load2[(nr - 1) % 4] += 1;
     for (int q = 0; q <= c0; q++) {
-        int b = 0;
-        for (int w = 1; w < nr; w++) {
+        int b = -1;
+        for (int w = 0; w < nr; w++) {
+            if (n[w] >= cap[w]) continue;
+            if (b < 0) {
+                b = w;
+                continue;
+            }
             const int lw = load2[w % 4], lb = load2[b % 4];
             if (lw < lb || (lw == lb && n[w] < n[b])) b = w;
         }
-        if (n[b] >= 6) {
+        if (b < 0 || n[b] >= 6) {
             s.ok = false;
             return s;
         }
