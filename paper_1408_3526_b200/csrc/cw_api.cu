@@ -113,9 +113,14 @@ struct cw_handle {
     bool chain = true;         // CW_CHAIN=0 turns it off
     bool last_static = false;  // the last fused launch used the static split
     // chained cw_submit: cuStreamWriteValue32 (driver entry point; null: not
-    // available -> event waits) and its flags [0] upload, [1] download
+    // available -> event waits) and its flags [0] upload, [1] download,
+    // [2] ring-slot copy of a resident frame (copy engine)
     CUresult (*write_value)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
     unsigned int *d_flags = nullptr;
+    // per ring slot: tag (frame + 1) of the flagged copy that filled it, 0 if
+    // it was filled in stream order; the next kernel's slot gets next_ring_tag
+    std::vector<unsigned int> ring_tag;
+    unsigned int next_ring_tag = 0;
     int nslots = 0;  // frame ring slots: max(mhat_z + 2, Mz + 1) (async upload spare; naive window)
     bool naive = false;  // spectrum backend: false = recursive (observer), true = naive window DFT
     int naive_grid = 0;
@@ -152,6 +157,10 @@ struct cw_handle {
 // frame chaining applies to the fused kernel with the recursive backend;
 // the in-kernel ring fill needs the delayed frame two launches back or more
 static bool chained(const cw_handle *h) { return h->chain && !h->generic && !h->naive && h->mhz >= 2; }
+
+#ifndef CW_RESIDENT_CE
+#define CW_RESIDENT_CE 1  // resident frames' ring copies on the copy engine (0: in the kernel prologue)
+#endif
 
 static int fail(cw_handle *h, int code, const std::string &msg)
 {
@@ -682,6 +691,7 @@ int cw_create(const cw_params *p, int32_t width, int32_t height, int32_t device,
     cudaMemsetAsync(h->d_state, 0, h->state_floats * 4, h->own);
     cudaMemsetAsync(h->d_that, 0, h->that_floats * 4, h->own);
     h->nslots = std::max(h->mhz + 2, h->mz + 1);
+    h->ring_tag.assign(h->nslots, 0u);
     cudaMemsetAsync(h->d_frames, 0, HW * 4 * h->nslots, h->own);
     cudaMemsetAsync(h->d_res, 0, HW * 4 * 2, h->own);
     cudaMemsetAsync(h->d_pred, 0, HW * 4 * 2, h->own);
@@ -712,9 +722,9 @@ int cw_create(const cw_params *p, int32_t width, int32_t height, int32_t device,
         void *fp = nullptr;
         cudaDriverEntryPointQueryResult q;
         if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &fp, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess && fp && cudaMalloc(&h->d_flags, 2 * sizeof(unsigned int)) == cudaSuccess) {
+            q == cudaDriverEntryPointSuccess && fp && cudaMalloc(&h->d_flags, 3 * sizeof(unsigned int)) == cudaSuccess) {
             h->write_value = reinterpret_cast<decltype(h->write_value)>(fp);
-            cudaMemsetAsync(h->d_flags, 0, 2 * sizeof(unsigned int), h->own);
+            cudaMemsetAsync(h->d_flags, 0, 3 * sizeof(unsigned int), h->own);
         }
         cudaGetLastError();
     }
@@ -863,7 +873,7 @@ struct FlagWants {
 
 static int run_frame(cw_handle *h, cudaStream_t s, int32_t *ready, int64_t *frame_index, float *res_o = nullptr,
                      float *pred_o = nullptr, uint8_t *vidx_o = nullptr, const float *frame_src = nullptr,
-                     bool chain = false, const FlagWants *flags = nullptr)
+                     bool chain = false, const FlagWants *flags = nullptr, bool ring_fill = true)
 {
     // chain: static split, and a programmatic dependent launch when the
     // previous fused launch was static too (done[] then names the same
@@ -926,10 +936,23 @@ static int run_frame(cw_handle *h, cudaStream_t s, int32_t *ready, int64_t *fram
             a.down_want = flags->down_want;
         }
     }
-    if (frame_src) {  // chained push: the kernel reads the caller's frame and fills the slot
-        a.ring_dst = const_cast<float *>(a.frame);
+    if (frame_src) {  // chained resident frame: the kernel reads the caller's frame (x stage) ...
+        if (ring_fill)  // ... and fills its ring slot itself (else a copy-engine copy does, flagged)
+            a.ring_dst = const_cast<float *>(a.frame);
         a.frame = frame_src;
     }
+    // the delayed frame's slot, if a flagged copy filled it: wait for the flag
+    a.ring_flag = nullptr;
+    a.ring_want = 0;
+    if (rd && h->d_flags) {
+        const unsigned int tag = h->ring_tag[(size_t)((n - h->mhz) % h->nslots)];
+        if (tag) {
+            a.ring_flag = h->d_flags + 2;
+            a.ring_want = tag;
+        }
+    }
+    h->ring_tag[(size_t)(n % h->nslots)] = h->next_ring_tag;
+    h->next_ring_tag = 0;
     a.det_tau = h->det_tau;
     a.det_cap = h->det_cap;
     if (h->det_on && rd) {
@@ -1037,6 +1060,7 @@ static int run_frame(cw_handle *h, cudaStream_t s, int32_t *ready, int64_t *fram
         h->last_static = a.work == nullptr;
         h->seq = a.seq;
     }
+    CW_CUDA(h, cudaEventRecord(h->ev_k[n % cw_handle::NEV], s));  // ring-slot reuse order (resident copies)
     if (h->timing)
         CW_CUDA(h, cudaEventRecord(e1, s));
     if (a.det) {  // results to the pinned mirror of this frame (ordered on s)
@@ -1409,6 +1433,19 @@ static int submit_device_impl(cw_handle *h, const float *frame_dev, float *resid
     // fills its ring slot itself, so consecutive frame kernels overlap
     // (chained); without chaining it is copied as cw_submit_device's
     const bool resident = resident_frame && chained(h) && slot != frame_dev;
+    // the ring slot (read as the delayed frame m^_z frames later) filled by a
+    // copy-engine copy on the upload stream after the kernel that last read
+    // the slot (n - 2 or earlier), flagged for the kernel that reads it
+    const bool ce_copy = resident && h->write_value && CW_RESIDENT_CE;
+    if (ce_copy) {
+        if (n >= 2)
+            CW_CUDA(h, cudaStreamWaitEvent(h->up, h->ev_k[(n - 2) % cw_handle::NEV], 0));
+        CW_CUDA(h, cudaMemcpyAsync(slot, frame_dev, HW * 4, cudaMemcpyDeviceToDevice, h->up));
+        if (h->write_value(reinterpret_cast<CUstream>(h->up), reinterpret_cast<CUdeviceptr>(h->d_flags + 2),
+                           (unsigned int)(n + 1), 0) != CUDA_SUCCESS)
+            return fail(h, CW_ERR_CUDA, "cuStreamWriteValue32 failed");
+        h->next_ring_tag = (unsigned int)(n + 1);
+    }
     if (!resident) {
         cudaStream_t ps = reinterpret_cast<cudaStream_t>(producer);
         CW_CUDA(h, cudaEventRecord(h->ev_up[e], ps));
@@ -1438,7 +1475,7 @@ static int submit_device_impl(cw_handle *h, const float *frame_dev, float *resid
     int64_t fi = -1;
     const size_t set = (size_t)(n & 1);
     int rc = run_frame(h, h->own, &rd, &fi, nullptr, nullptr, nullptr, resident ? frame_dev : nullptr, resident,
-                       use_fw ? &fw : nullptr);
+                       use_fw ? &fw : nullptr, !ce_copy);
     if (rc != CW_OK)
         return rc;
     CW_CUDA(h, cudaEventRecord(h->ev_k[e], h->own));
@@ -1634,7 +1671,9 @@ int cw_restore(cw_handle *h, const void *src, size_t bytes)
     h->have_that = hd.have_that != 0;
     // the submit flags are tagged with frame numbers: restart them
     if (h->d_flags)
-        CW_CUDA(h, cudaMemset(h->d_flags, 0, 2 * sizeof(unsigned int)));
+        CW_CUDA(h, cudaMemset(h->d_flags, 0, 3 * sizeof(unsigned int)));
+    std::fill(h->ring_tag.begin(), h->ring_tag.end(), 0u);
+    h->next_ring_tag = 0;
     for (bool &f : h->dl_flagged)
         f = false;
     for (bool &f : h->dl_any)
@@ -1687,6 +1726,12 @@ int cw_set_backend(cw_handle *h, int32_t naive)
                                                                  h->fn.naive_smem));
         CW_CUDA(h, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device));
         h->naive_grid = std::max(1, occ * sms);
+    }
+    // the naive kernel reads Mz ring frames without waiting on flags: any
+    // flagged (copy-engine) ring copy must be complete
+    if (naive && h->up) {
+        CW_CUDA(h, cudaStreamSynchronize(h->up));
+        std::fill(h->ring_tag.begin(), h->ring_tag.end(), 0u);
     }
     h->naive = naive != 0;
     return CW_OK;

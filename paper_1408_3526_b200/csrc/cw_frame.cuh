@@ -269,6 +269,10 @@ struct FrameArgs {
     // for up_flag >= up_want and down_flag >= down_want (nullable)
     const unsigned int *up_flag, *down_flag;
     unsigned int up_want, down_want;
+    // the delayed frame's ring slot filled by a flagged copy (resident
+    // frames, copy engine): wait for ring_flag >= ring_want (nullable)
+    const unsigned int *ring_flag;
+    unsigned int ring_want;
 };
 
 // Fused "final threshold" and the ground-truth-free metrics of
@@ -658,9 +662,10 @@ cw_frame_kernel(const FrameArgs a, const Tables t)
 #ifdef CW_PHASE_TIMING
     if (threadIdx.x == 0 && blockIdx.x < 1024) cw_cta_span[a.seq & 1][blockIdx.x][1] = cw_gtimer();
 #endif
-    if ((a.up_flag || a.down_flag) && threadIdx.x == G::NTHREADS - 32) {
+    if ((a.up_flag || a.down_flag || a.ring_flag) && threadIdx.x == G::NTHREADS - 32) {
         if (a.up_flag) chain_wait(a.up_flag, a.up_want);
         if (a.down_flag) chain_wait(a.down_flag, a.down_want);
+        if (a.ring_flag) chain_wait(a.ring_flag, a.ring_want);
     }
     if (a.ring_dst) {
         // every CTA of launch seq - 2 through: all flags read at once (relaxed,
