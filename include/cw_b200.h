@@ -128,11 +128,13 @@ int cw_submit_device(cw_handle *h, const float *frame_dev, float *residual, floa
  * cw_submit for a frame that is already complete in device memory and stays
  * unchanged until cw_wait(ticket) returns (resident inputs, e.g. a frame
  * buffer filled before the stream starts).  No producer stream is joined
- * and no copy is enqueued: the frame kernel reads `frame_dev` and fills its
- * ring slot itself, and consecutive frame kernels are chained (programmatic
- * dependent launch; each CTA waits only for its own units of the previous
- * frame), so a frame's kernel starts in the SM slots the
- * previous frame's early CTAs free.  Host output buffers may be NULL (the
+ * and nothing is enqueued between frame kernels: the frame kernel reads
+ * `frame_dev` directly, its ring slot (the delayed frame of a later kernel)
+ * is filled by a copy-engine copy on the upload stream that the later
+ * kernel waits for by a flag, and consecutive frame kernels are chained
+ * (programmatic dependent launch; each CTA waits only for its own units of
+ * the previous frame), so a frame's kernel starts in
+ * the SM slots the previous frame's early CTAs free.  Host output buffers may be NULL (the
  * results stay on the device: cw_device_outputs after cw_wait).  Results are
  * bit-identical to cw_push_device's with the static work split.
  * (Not in the reference: its frames are host arrays, pipeline.py:201.)

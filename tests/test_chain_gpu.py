@@ -1,6 +1,7 @@
 """Frame chaining: consecutive frame kernels overlap
-(programmatic dependent launch, per-CTA completion flags, in-kernel ring
-fill for resident frames, stream-memory-write flags for cw_submit).  The
+(programmatic dependent launch, per-CTA completion flags, flagged
+copy-engine ring copies for resident frames, stream-memory-write flags for
+cw_submit uploads and downloads).  The
 chained entry points must give bit-identical results to plain, fully
 serialised launches with the same (static) work split, across frame sizes
 whose CTA runs are short (C2-like) and long, mixed entry points, and a
