@@ -721,7 +721,8 @@ int cw_create(const cw_params *p, int32_t width, int32_t height, int32_t device,
     {
         void *fp = nullptr;
         cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &fp, cudaEnableDefault, &q) == cudaSuccess &&
+        if (!std::getenv("CW_NO_MEMOPS") &&  // (test knob: the event-wait fallback)
+            cudaGetDriverEntryPoint("cuStreamWriteValue32", &fp, cudaEnableDefault, &q) == cudaSuccess &&
             q == cudaDriverEntryPointSuccess && fp && cudaMalloc(&h->d_flags, 3 * sizeof(unsigned int)) == cudaSuccess) {
             h->write_value = reinterpret_cast<decltype(h->write_value)>(fp);
             cudaMemsetAsync(h->d_flags, 0, 3 * sizeof(unsigned int), h->own);

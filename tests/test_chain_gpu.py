@@ -282,3 +282,18 @@ def test_process_resident_matches_process_frame(params, monkeypatch):
         assert np.array_equal(x.residual, y.residual)
         assert np.array_equal(x.prediction, y.prediction)
         assert np.array_equal(x.velocity.indices, y.velocity.indices)
+
+
+@pytest.mark.parametrize("mode", ["resident", "submit"])
+def test_chain_without_stream_memory_ops(params, mode, monkeypatch):
+    """The fallback when cuStreamWriteValue32 is unavailable: resident
+    frames copy their ring slot in the kernel prologue, cw_submit waits on
+    events; results unchanged."""
+    frames = _frames(20, 128, 192, seed=17)
+    seen_a, snap_a, _ = _run(params, frames, ["push"] if mode == "resident" else ["submit"], monkeypatch,
+                             chain=False)
+    monkeypatch.setenv("CW_NO_MEMOPS", "1")
+    seen_b, snap_b, _ = _run(params, frames, [mode], monkeypatch, chain=True)
+    assert np.array_equal(snap_a, snap_b)
+    for k in seen_b:
+        assert np.array_equal(seen_a[k], seen_b[k]), k
